@@ -1,0 +1,199 @@
+/*
+ * psn.h -- C ABI of the B200-native Parallel SurfaceNets hot path.
+ *
+ * Library: paper_2401_14906_b200/libpsn.so (sm_100a CUDA kernels + this ABI).
+ * Every entry point follows the paper's statement of the problem
+ * (/root/reference/PAPER.md, cited "P:<line>"):
+ *   input  = a label volume with spacing/origin, a label set L
+ *            whose complement is background B, an iteration count, a
+ *            relaxation factor lambda and a constraint distance;
+ *   output = points, quads, region-adjacency two-tuples, smoothing stencils
+ *             and optionally triangles.
+ *
+ * Conventions (all calls):
+ *   - Plain pointers and sizes only; no exceptions cross the ABI.  Every call
+ *     returns a psn_status; psn_last_error(ctx) gives a text message.
+ *   - Device pointers are caller-owned (the library never allocates device
+ *     memory).  Work is enqueued on the caller's CUDA stream `stream`
+ *     (a cudaStream_t passed as void*); calls are stream-ordered and never
+ *     synchronise the device, except where stated (PSN_COUNT reads 3 totals).
+ *   - Arguments are validated before any launch; on an error nothing is launched.
+ *   - Outputs are bit-identical across runs, launch configurations and rank
+ *     counts (after rank-order concatenation): no atomics on output values.
+ *   - Label volumes are x-fastest: idx = i + M*(j + N*(k - z_lo)).
+ *   - Ids are uint32 (reading Q20); totals >= 2^32 give PSN_ERR_OVERFLOW.
+ *   - Background in two-tuples is PSN_BACKGROUND (reading Q3).
+ */
+#ifndef PSN_H
+#define PSN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSN_BACKGROUND 0xFFFFFFFFu
+
+typedef enum {
+    PSN_OK = 0,
+    PSN_ERR_ARG = 1,        /* bad argument: null pointer, dims < 2, spacing <= 0, lambda not in [0,1], d < 0, T < 0, bad slab bounds */
+    PSN_ERR_LABELS = 2,     /* empty label set without all_nonzero, or PSN_BACKGROUND in the set */
+    PSN_ERR_OVERFLOW = 3,   /* P, Q or S would reach 2^32: totals are still reported */
+    PSN_ERR_CAPACITY = 4,   /* output capacities too small: totals reported, nothing emitted */
+    PSN_ERR_STATE = 5,      /* PSN_EMIT without a matching PSN_COUNT on this workspace */
+    PSN_ERR_CUDA = 6        /* a CUDA runtime error (message in psn_last_error) */
+} psn_status;
+
+typedef enum { PSN_U8 = 1, PSN_U16 = 2, PSN_U32 = 4 } psn_dtype;
+
+typedef enum {
+    PSN_TRI_FIXED_02 = 0,   /* "greedy": always diagonal 0-2 (reading Q13) */
+    PSN_TRI_SHORTEST = 1    /* shorter diagonal, ties -> 0-2 */
+} psn_tri;
+
+enum { PSN_COUNT = 1, PSN_EMIT = 2 };
+
+typedef struct psn_ctx psn_ctx;   /* opaque HOST object: device id, SM count, last error */
+
+/*
+ * Label volume (device memory, caller-owned).  One process may hold a z-slab
+ * of the global volume (multi-GPU): lattice slices [z_lo, z_hi)
+ * are present in `labels`, and this call owns voxel layers [own_k0, own_k1).
+ * Required: z_lo <= max(own_k0-1, 0) and z_hi >= min(own_k1+1, O-1) + 1,
+ * i.e. a one-slice halo on each interior side.  Single GPU: z_lo=0, z_hi=O,
+ * own_k0=0, own_k1=O-1.
+ */
+typedef struct {
+    const void *labels;
+    psn_dtype dtype;
+    int64_t dims[3];        /* GLOBAL lattice points M, N, O; each >= 2 */
+    double spacing[3];      /* world units per lattice step, > 0 */
+    double origin[3];       /* world position of lattice point (0,0,0) */
+    int64_t z_lo, z_hi;
+    int64_t own_k0, own_k1;
+} psn_volume;
+
+/*
+ * Selected label set L (HOST memory).  all_nonzero != 0 selects every
+ * non-zero value (reading Q2) and ignores `values`.  Otherwise values need
+ * not be sorted or unique; values that cannot occur in the dtype are ignored.
+ */
+typedef struct {
+    const uint32_t *values;
+    int64_t count;
+    int all_nonzero;
+} psn_labels;
+
+/*
+ * Extracted mesh (device arrays, caller-owned).  Point-indexed arrays use a
+ * WINDOW index  w = id - (first_point - halo_lo_points):
+ *   points          float[halo_lo + P + halo_hi][3]  voxel centres
+ *                   fl32(origin + (idx + 0.5) * spacing) computed in fp64 (C-3);
+ *                   includes the points of the halo layers own_k0-1 / own_k1
+ *                   (needed by smoothing and triangulation on a slab)
+ *   face_masks      uint8[P]      own points: bit f set iff stencil holds face f
+ *                                 (f = -z,-y,-x,+x,+y,+z)
+ *   stencil_offsets uint32[P+1]   own points: CSR row starts (global, start at first_stencil)
+ *   stencil_ids     uint32[S]     neighbour point ids, face order = ascending id
+ *   quads           uint32[Q][4]  point ids, voxel-major then x<y<z (reading Q4/Q6)
+ *   pairs           uint32[Q][2]  (cls at edge origin, cls at far end)
+ * Capacities cap_* count elements of the leading dimension (points: window
+ * entries).  n_* / halo_* are written by PSN_COUNT; first_* are inputs to
+ * PSN_EMIT (global offsets from the cross-rank exclusive scan, 0 on one GPU).
+ */
+typedef struct {
+    float *points;
+    uint32_t *quads;
+    uint32_t *pairs;
+    uint32_t *stencil_offsets;
+    uint32_t *stencil_ids;
+    uint8_t *face_masks;
+    int64_t cap_points, cap_quads, cap_stencil;
+    int64_t n_points, n_quads, n_stencil;        /* out: this call's own totals */
+    int64_t halo_lo_points, halo_hi_points;      /* out: points in layers own_k0-1 / own_k1 */
+    int64_t first_point, first_quad, first_stencil;  /* in (EMIT) */
+} psn_mesh;
+
+psn_status psn_ctx_create(int device, psn_ctx **out);
+void psn_ctx_destroy(psn_ctx *ctx);
+const char *psn_last_error(const psn_ctx *ctx);
+const char *psn_status_string(psn_status s);
+
+/* Bytes of device workspace psn_extract needs for this volume (row counts,
+ * offsets, trims, point bit-planes, scan tile status, label bitset). */
+psn_status psn_extract_workspace(const psn_volume *vol, size_t *bytes);
+
+/*
+ * Surface extraction (PAPER sec 2.3, Passes 1-4).
+ *   phase & PSN_COUNT: Passes 1-3 -- per voxel row point/quad/stencil counts,
+ *       trims and point bit-planes (k_count), then the row-wise exclusive scan
+ *       (k_scan).  Reads 3 totals back (one stream synchronisation) into
+ *       mesh->n_points/n_quads/n_stencil/halo_*.  PSN_ERR_OVERFLOW if any total
+ *       reaches 2^32.
+ *   phase == PSN_EMIT: Pass 4 (k_emit) into the caller's arrays, using the
+ *       scan kept in `ws` by the preceding PSN_COUNT.  Capacities are checked on
+ *       the host against the counted totals (PSN_ERR_CAPACITY, nothing launched).
+ *   phase == PSN_COUNT|PSN_EMIT: fully stream-ordered, no host sync: the emit
+ *       kernel reads the device totals and writes nothing if they exceed the
+ *       capacities; the totals are NOT written back to *mesh (call
+ *       psn_mesh_totals later to read them and the device status word).
+ * ws must stay untouched between COUNT and EMIT.
+ */
+psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *labels,
+                       psn_mesh *mesh, unsigned phase, void *ws, size_t ws_bytes, void *stream);
+
+/* Synchronising read of the totals and capacity status left in ws by the
+ * last psn_extract (for the PSN_COUNT|PSN_EMIT path).  Returns
+ * PSN_ERR_CAPACITY if that emission was skipped. */
+psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh,
+                           const void *ws, size_t ws_bytes, void *stream);
+
+/* Workspace of psn_smooth: two fp32 [n_window][3] index-space offset buffers. */
+psn_status psn_smooth_workspace(int64_t n_points_window, size_t *bytes);
+
+/*
+ * Constrained Laplacian smoothing (Eq. 1) with double buffering
+ * (P:94), `iterations` Jacobi steps on the caller's stream, then world
+ * coordinates of every window point into out[w][3]:
+ *   per own point with N = deg > 0:  o' = clamp(o + lambda * mean_j(p_j - p_i)/s, -d, +d)
+ * computed on fp32 index-space offsets o from the exact voxel-centre anchor;
+ * out = fl32(anchor64 + s * o).  iterations = 0 or lambda = 0 gives the anchors.
+ * Single GPU / whole volume only (halo layers empty); a slab uses
+ * psn_smooth_step below.  constraint_distance d is in voxel units (box
+ * half-width d*s per axis, readings Q9/Q10).
+ */
+psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, float *out,
+                      int32_t iterations, float relaxation, float constraint_distance,
+                      void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * One Jacobi iteration over the own points of a slab: reads the window offset
+ * buffer src[n_window][3] (halo entries must hold the neighbours' current
+ * values), writes the own entries of dst.  Between steps the caller exchanges
+ * the boundary layers (multi-GPU).  src == NULL means "all offsets zero"
+ * (first iteration from the anchors).
+ */
+psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const float *src, float *dst,
+                           float relaxation, float constraint_distance, void *stream);
+
+/* World coordinates of window entries [w0, w1) from offsets (NULL = anchors). */
+psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
+                               const float *offsets, int64_t w0, int64_t w1, float *out, void *stream);
+
+/*
+ * Triangulation: quad q -> triangles 2q, 2q+1; tris uint32[2Q][3];
+ * the two-tuple of triangle t is pairs[t/2].  `points` is window-indexed
+ * (as psn_mesh.points), typically the smoothed output of psn_smooth.
+ */
+psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *points, psn_tri tri,
+                           uint32_t *tris, void *stream);
+
+/* Number of kernel launches the last call on this ctx enqueued (bench.py's gpu_launches). */
+int64_t psn_launch_count(const psn_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSN_H */

@@ -1,0 +1,126 @@
+// k_smooth.cuh -- constrained Laplacian smoothing (PAPER Eq. 1) with
+// double buffering, and shortest-diagonal triangulation.
+//
+// Positions are fp32 INDEX-SPACE OFFSETS o from each point's exact voxel-centre
+// anchor: the world difference p_j - p_i of face neighbours
+// is s * (e_f + o_j - o_i) with e_f = +-1 along the face axis, and the box
+// constraint (reading Q10) is |o_a| <= d.  So one Jacobi step is
+//     o' = clamp(o + lambda * (1/N) * sum_f (e_f + o_j - o_i), -d, d)
+// per axis, exactly Eq. 1 divided by s (box-mode Jacobi is per-axis affine
+// equivariant, reading Q11).  The face of the n-th CSR entry is the n-th set
+// bit of the 6-bit face mask (CSR order = face order, reading Q7).
+// World output = fl32(anchor64 + s*o) with anchor64 recovered exactly from the
+// fp32 voxel centre (idx = rint((p - origin)/s - 0.5)).
+#pragma once
+#include "psn_common.cuh"
+
+namespace psn {
+
+struct SmoothArgs {
+    const float *src;          // window offsets [n_window][3]; NULL = all zero
+    float *dst;                // window offsets (own entries written)
+    float *world;              // if non-NULL: write world coordinates here instead of dst
+    const uint8_t *fmask;      // own points
+    const uint32_t *csr_off;   // own points (global values)
+    const uint32_t *csr_ids;   // global ids
+    const float *points;       // window anchors (fp32 voxel centres), for the world output
+    int64_t n_own;
+    uint32_t halo_lo;          // window index of the first own point
+    uint32_t win_base;         // global id of window index 0
+    uint32_t first_stencil;
+    float lambda, d;
+    double sp[3], org[3];
+};
+
+__device__ __forceinline__ double anchor64_from(float p, double org, double sp) {
+    const double idx = rint(__dsub_rn(__ddiv_rn(__dsub_rn((double)p, org), sp), 0.5));
+    return __dadd_rn(org, __dmul_rn(__dadd_rn(idx, 0.5), sp));
+}
+
+__device__ __forceinline__ float world_of(float p, float o, double org, double sp) {
+    return __double2float_rn(__dadd_rn(anchor64_from(p, org, sp), __dmul_rn(sp, (double)o)));
+}
+
+__global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_own;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = a.halo_lo + i;
+        float ox = 0.f, oy = 0.f, oz = 0.f;
+        if (a.src) { ox = a.src[3 * w]; oy = a.src[3 * w + 1]; oz = a.src[3 * w + 2]; }
+        uint32_t f = a.fmask[i];
+        float nx = ox, ny = oy, nz = oz;
+        if (f) {
+            const uint32_t s0 = a.csr_off[i] - a.first_stencil;
+            float sx = 0.f, sy = 0.f, sz = 0.f;
+            int n = 0;
+            while (f) {
+                const int face = __ffs(f) - 1;
+                f &= f - 1;
+                const int64_t wj = (int64_t)(a.csr_ids[s0 + n] - a.win_base);
+                ++n;
+                float dx = 0.f, dy = 0.f, dz = 0.f;
+                if (a.src) { dx = a.src[3 * wj] - ox; dy = a.src[3 * wj + 1] - oy; dz = a.src[3 * wj + 2] - oz; }
+                // e_f: faces -z,-y,-x,+x,+y,+z
+                switch (face) {
+                    case 0: dz -= 1.f; break;
+                    case 1: dy -= 1.f; break;
+                    case 2: dx -= 1.f; break;
+                    case 3: dx += 1.f; break;
+                    case 4: dy += 1.f; break;
+                    default: dz += 1.f; break;
+                }
+                sx += dx; sy += dy; sz += dz;
+            }
+            const float fn = (float)n;   // m = sum / N, q = o + lambda * m, clamp (readings Q8, Q9)
+            nx = fminf(fmaxf(__fadd_rn(ox, __fmul_rn(a.lambda, __fdiv_rn(sx, fn))), -a.d), a.d);
+            ny = fminf(fmaxf(__fadd_rn(oy, __fmul_rn(a.lambda, __fdiv_rn(sy, fn))), -a.d), a.d);
+            nz = fminf(fmaxf(__fadd_rn(oz, __fmul_rn(a.lambda, __fdiv_rn(sz, fn))), -a.d), a.d);
+        }
+        if (a.world) {
+            a.world[3 * w + 0] = world_of(a.points[3 * w + 0], nx, a.org[0], a.sp[0]);
+            a.world[3 * w + 1] = world_of(a.points[3 * w + 1], ny, a.org[1], a.sp[1]);
+            a.world[3 * w + 2] = world_of(a.points[3 * w + 2], nz, a.org[2], a.sp[2]);
+        } else {
+            a.dst[3 * w + 0] = nx; a.dst[3 * w + 1] = ny; a.dst[3 * w + 2] = nz;
+        }
+    }
+}
+
+// World coordinates of window entries [w0, w1) from offsets (NULL = anchors).
+__global__ void __launch_bounds__(256) k_finalize(const float *offs, const float *points, float *out,
+                                                  int64_t w0, int64_t w1, double sx, double sy, double sz,
+                                                  double ox, double oy, double oz) {
+    for (int64_t w = w0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < w1;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const float o0 = offs ? offs[3 * w] : 0.f, o1 = offs ? offs[3 * w + 1] : 0.f, o2 = offs ? offs[3 * w + 2] : 0.f;
+        out[3 * w + 0] = world_of(points[3 * w + 0], o0, ox, sx);
+        out[3 * w + 1] = world_of(points[3 * w + 1], o1, oy, sy);
+        out[3 * w + 2] = world_of(points[3 * w + 2], o2, oz, sz);
+    }
+}
+
+// Triangulation: quad q -> tris 2q, 2q+1 (reading Q13 / C-8: diagonals from the
+// fp32 points in fp64, differences, squares, sum x+y+z; ties -> 0-2).
+__global__ void __launch_bounds__(256) k_triangulate(const uint32_t *quads, const float *points, uint32_t *tris,
+                                                     int64_t nQ, uint32_t win_base, int shortest) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nQ; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(quads) + q);
+        bool d02 = true;
+        if (shortest) {
+            const float *p0 = points + 3 * (int64_t)(v.x - win_base), *p1 = points + 3 * (int64_t)(v.y - win_base);
+            const float *p2 = points + 3 * (int64_t)(v.z - win_base), *p3 = points + 3 * (int64_t)(v.w - win_base);
+            double a0 = __dsub_rn((double)p2[0], (double)p0[0]), a1 = __dsub_rn((double)p2[1], (double)p0[1]);
+            double a2 = __dsub_rn((double)p2[2], (double)p0[2]);
+            double b0 = __dsub_rn((double)p3[0], (double)p1[0]), b1 = __dsub_rn((double)p3[1], (double)p1[1]);
+            double b2 = __dsub_rn((double)p3[2], (double)p1[2]);
+            const double da = __dadd_rn(__dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)), __dmul_rn(a2, a2));
+            const double db = __dadd_rn(__dadd_rn(__dmul_rn(b0, b0), __dmul_rn(b1, b1)), __dmul_rn(b2, b2));
+            d02 = da <= db;
+        }
+        uint2 *t = reinterpret_cast<uint2 *>(tris + 6 * q);
+        if (d02) { t[0] = make_uint2(v.x, v.y); t[1] = make_uint2(v.z, v.x); t[2] = make_uint2(v.z, v.w); }
+        else     { t[0] = make_uint2(v.x, v.y); t[1] = make_uint2(v.w, v.y); t[2] = make_uint2(v.z, v.w); }
+    }
+}
+
+}  // namespace psn

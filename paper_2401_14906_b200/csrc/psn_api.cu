@@ -1,0 +1,491 @@
+// psn_api.cu -- host side of the C ABI declared in include/psn.h.
+//
+// Validation, workspace layout, label-set preparation and stream-ordered
+// launches of the sm_100a kernels:
+//   psn_extract(COUNT) -> k_count (Passes 1-3 counting) -> k_scan (Pass 3 prefix sum)
+//   psn_extract(EMIT)  -> k_emit  (Pass 4)
+//   psn_smooth         -> k_smooth x T (Eq. 1, double-buffered; last step fused with finalize)
+//   psn_triangulate    -> k_triangulate
+// The library never allocates device memory; every buffer is the caller's.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "psn.h"
+#include "k_count.cuh"
+#include "k_emit.cuh"
+#include "k_scan.cuh"
+#include "k_smooth.cuh"
+
+using namespace psn;
+
+struct psn_ctx {
+    int device = 0;
+    int sms = 148;
+    std::string err;
+    int64_t launches = 0;
+    std::vector<uint32_t> label_host;     // bitset or sorted list kept alive for async copies
+    const void *counted_ws = nullptr;     // workspace holding a valid COUNT result
+    int64_t counted_sig[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace {
+
+psn_status fail(psn_ctx *ctx, psn_status s, const char *fmt, ...) {
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return s;
+}
+
+psn_status cuda_check(psn_ctx *ctx, const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, PSN_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+    return PSN_OK;
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+    int64_t M, N, O, kA, kB, R, W4, nTiles;
+    size_t hdr, tiles, cntP, cntQ, cntS, offP, offQ, offS, trim, pmask, labels, total;
+};
+
+constexpr int64_t kMaxList = 65536;   // u32 label-subset capacity in the workspace
+
+psn_status layout(psn_ctx *ctx, const psn_volume *v, Layout *L) {
+    if (!v) return fail(ctx, PSN_ERR_ARG, "volume is NULL");
+    const int64_t M = v->dims[0], N = v->dims[1], O = v->dims[2];
+    if (M < 2 || N < 2 || O < 2) return fail(ctx, PSN_ERR_ARG, "dims must be >= 2 (got %lld %lld %lld)",
+                                             (long long)M, (long long)N, (long long)O);
+    if (M > (1ll << 31) || N > (1ll << 31) || O > (1ll << 31)) return fail(ctx, PSN_ERR_ARG, "dims too large");
+    if (v->dtype != PSN_U8 && v->dtype != PSN_U16 && v->dtype != PSN_U32)
+        return fail(ctx, PSN_ERR_ARG, "dtype must be PSN_U8, PSN_U16 or PSN_U32");
+    for (int a = 0; a < 3; ++a)
+        if (!(v->spacing[a] > 0.0)) return fail(ctx, PSN_ERR_ARG, "spacing must be > 0");
+    if (v->own_k0 < 0 || v->own_k1 > O - 1 || v->own_k0 >= v->own_k1)
+        return fail(ctx, PSN_ERR_ARG, "need 0 <= own_k0 < own_k1 <= O-1");
+    L->M = M; L->N = N; L->O = O;
+    L->kA = v->own_k0 - (v->own_k0 > 0 ? 1 : 0);
+    L->kB = v->own_k1 + (v->own_k1 < O - 1 ? 1 : 0);
+    if (v->z_lo > L->kA || v->z_hi < L->kB + 1 || v->z_lo < 0 || v->z_hi > O)
+        return fail(ctx, PSN_ERR_ARG, "slab slices [%lld,%lld) must contain [%lld,%lld] (one-slice halos)",
+                    (long long)v->z_lo, (long long)v->z_hi, (long long)L->kA, (long long)L->kB);
+    L->R = (N - 1) * (L->kB - L->kA);
+    L->W4 = (M - 1 + 127) / 128;
+    L->nTiles = (L->R + kScanTile - 1) / kScanTile;
+    size_t off = 0;
+    L->hdr = off; off += align_up(sizeof(ScanHeader));
+    L->tiles = off; off += align_up(sizeof(TileStatus) * (size_t)L->nTiles);
+    L->cntP = off; off += align_up(4 * (size_t)L->R);
+    L->cntQ = off; off += align_up(4 * (size_t)L->R);
+    L->cntS = off; off += align_up(4 * (size_t)L->R);
+    L->offP = off; off += align_up(4 * (size_t)L->R);
+    L->offQ = off; off += align_up(4 * (size_t)L->R);
+    L->offS = off; off += align_up(4 * (size_t)L->R);
+    L->trim = off; off += align_up(8 * (size_t)L->R);
+    L->pmask = off; off += align_up(16 * (size_t)L->R * (size_t)L->W4);
+    L->labels = off;
+    off += align_up(v->dtype == PSN_U32 ? 4 * (size_t)kMaxList : 8192);
+    L->total = off;
+    return PSN_OK;
+}
+
+template <typename P> P *at(void *ws, size_t off) { return reinterpret_cast<P *>(static_cast<char *>(ws) + off); }
+
+// Label set -> device LabelSet (bitset for u8/u16, sorted list for u32).
+psn_status prepare_labels(psn_ctx *ctx, const psn_volume *v, const psn_labels *lab, void *ws, const Layout &L,
+                          cudaStream_t st, LabelSet *out, bool *anz) {
+    memset(out, 0, sizeof(*out));
+    if (!lab) return fail(ctx, PSN_ERR_ARG, "labels is NULL");
+    if (lab->all_nonzero) { *anz = true; return PSN_OK; }
+    *anz = false;
+    if (lab->count <= 0 || !lab->values) return fail(ctx, PSN_ERR_LABELS, "empty label set without all_nonzero");
+    for (int64_t n = 0; n < lab->count; ++n)
+        if (lab->values[n] == PSN_BACKGROUND) return fail(ctx, PSN_ERR_LABELS, "label set contains the background sentinel");
+    uint32_t *dev = at<uint32_t>(ws, L.labels);
+    if (v->dtype == PSN_U32) {
+        std::vector<uint32_t> s(lab->values, lab->values + lab->count);
+        std::sort(s.begin(), s.end());
+        s.erase(std::unique(s.begin(), s.end()), s.end());
+        if ((int64_t)s.size() > kMaxList) return fail(ctx, PSN_ERR_ARG, "u32 label subsets are limited to %lld values",
+                                                      (long long)kMaxList);
+        ctx->label_host = s;
+        if (!s.empty() && cudaMemcpyAsync(dev, ctx->label_host.data(), 4 * s.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return cuda_check(ctx, "label upload");
+        out->list = dev; out->n_list = (int64_t)s.size(); out->z = PSN_BACKGROUND; out->identity = 0;
+        return PSN_OK;
+    }
+    const uint32_t nvals = v->dtype == PSN_U8 ? 256u : 65536u;
+    ctx->label_host.assign(2048, 0u);
+    for (int64_t n = 0; n < lab->count; ++n) {
+        const uint32_t x = lab->values[n];
+        if (x < nvals) ctx->label_host[x >> 5] |= 1u << (x & 31);   // values outside the dtype are ignored
+    }
+    uint32_t z = nvals;
+    for (uint32_t x = 0; x < nvals; ++x)
+        if (!((ctx->label_host[x >> 5] >> (x & 31)) & 1u)) { z = x; break; }
+    if (cudaMemcpyAsync(dev, ctx->label_host.data(), 8192, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return cuda_check(ctx, "label upload");
+    out->bits = dev; out->z = z; out->identity = (z == nvals) ? 1 : 0;
+    return PSN_OK;
+}
+
+__global__ void k_init_multixt(uint32_t *cp, uint32_t *cq, uint32_t *cs, int2 *trim, int64_t R) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+        cp[r] = 0; cq[r] = 0; cs[r] = 0; trim[r] = make_int2(0x7fffffff, 0);
+    }
+}
+
+template <typename T, bool ANZ, bool VEC>
+void launch_count(const CountArgs &ca, int64_t blocks, int threads, cudaStream_t st) {
+    constexpr int TJ = sizeof(T) == 1 ? 8 : (sizeof(T) == 2 ? 4 : 2);
+    k_count<T, TJ, ANZ, VEC><<<(unsigned)blocks, threads, 0, st>>>(ca);
+}
+
+template <typename T>
+int tj_of() { return sizeof(T) == 1 ? 8 : (sizeof(T) == 2 ? 4 : 2); }
+
+template <typename T>
+void dispatch_count(const CountArgs &ca, bool anz, bool vec, int64_t blocks, int threads, cudaStream_t st) {
+    if (anz) { if (vec) launch_count<T, true, true>(ca, blocks, threads, st); else launch_count<T, true, false>(ca, blocks, threads, st); }
+    else     { if (vec) launch_count<T, false, true>(ca, blocks, threads, st); else launch_count<T, false, false>(ca, blocks, threads, st); }
+}
+
+template <typename T>
+void dispatch_emit(const EmitArgs &ea, bool anz, bool vec, int64_t blocks, cudaStream_t st) {
+    if (anz) { if (vec) k_emit<T, true, true><<<(unsigned)blocks, 256, 0, st>>>(ea); else k_emit<T, true, false><<<(unsigned)blocks, 256, 0, st>>>(ea); }
+    else     { if (vec) k_emit<T, false, true><<<(unsigned)blocks, 256, 0, st>>>(ea); else k_emit<T, false, false><<<(unsigned)blocks, 256, 0, st>>>(ea); }
+}
+
+void signature(const psn_volume *v, int64_t sig[6]) {
+    sig[0] = v->dims[0]; sig[1] = v->dims[1]; sig[2] = v->dims[2];
+    sig[3] = v->own_k0; sig[4] = v->own_k1; sig[5] = (int64_t)(intptr_t)v->labels;
+}
+
+psn_status read_totals(psn_ctx *ctx, const psn_volume *v, const Layout &L, const void *ws, psn_mesh *mesh,
+                       cudaStream_t st, uint32_t *emit_status) {
+    ScanHeader h;
+    if (cudaMemcpyAsync(&h, static_cast<const char *>(ws) + L.hdr, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return cuda_check(ctx, "totals read-back");
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(ctx, "totals sync");
+    const bool has_lo = L.kA < v->own_k0, has_hi = L.kB > v->own_k1;
+    const uint64_t halo_lo = has_lo ? h.halo_lo : 0;
+    const uint64_t before_hi = has_hi ? h.halo_hi : h.total[0];
+    mesh->halo_lo_points = (int64_t)halo_lo;
+    mesh->halo_hi_points = (int64_t)(h.total[0] - before_hi);
+    mesh->n_points = (int64_t)(before_hi - halo_lo);
+    mesh->n_quads = (int64_t)h.total[1];
+    mesh->n_stencil = (int64_t)h.total[2];
+    if (emit_status) *emit_status = h.emit_status;
+    const uint64_t lim = 1ull << 32;
+    if (h.total[0] >= lim || h.total[1] >= lim || h.total[2] >= lim)
+        return fail(ctx, PSN_ERR_OVERFLOW, "output exceeds 32-bit ids: P=%llu Q=%llu S=%llu",
+                    (unsigned long long)h.total[0], (unsigned long long)h.total[1], (unsigned long long)h.total[2]);
+    return PSN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+psn_status psn_ctx_create(int device, psn_ctx **out) {
+    if (!out) return PSN_ERR_ARG;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        *out = nullptr;
+        return PSN_ERR_CUDA;
+    }
+    psn_ctx *c = new psn_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    *out = c;
+    return PSN_OK;
+}
+
+void psn_ctx_destroy(psn_ctx *ctx) { delete ctx; }
+
+const char *psn_last_error(const psn_ctx *ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+const char *psn_status_string(psn_status s) {
+    switch (s) {
+        case PSN_OK: return "PSN_OK";
+        case PSN_ERR_ARG: return "PSN_ERR_ARG";
+        case PSN_ERR_LABELS: return "PSN_ERR_LABELS";
+        case PSN_ERR_OVERFLOW: return "PSN_ERR_OVERFLOW";
+        case PSN_ERR_CAPACITY: return "PSN_ERR_CAPACITY";
+        case PSN_ERR_STATE: return "PSN_ERR_STATE";
+        case PSN_ERR_CUDA: return "PSN_ERR_CUDA";
+    }
+    return "unknown";
+}
+
+int64_t psn_launch_count(const psn_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+psn_status psn_extract_workspace(const psn_volume *vol, size_t *bytes) {
+    if (!bytes) return PSN_ERR_ARG;
+    Layout L;
+    psn_status s = layout(nullptr, vol, &L);
+    if (s != PSN_OK) return s;
+    *bytes = L.total;
+    return PSN_OK;
+}
+
+psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *labels, psn_mesh *mesh,
+                       unsigned phase, void *ws, size_t ws_bytes, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    Layout L;
+    psn_status s = layout(ctx, vol, &L);
+    if (s != PSN_OK) return s;
+    if (!mesh) return fail(ctx, PSN_ERR_ARG, "mesh is NULL");
+    if (!vol->labels) return fail(ctx, PSN_ERR_ARG, "labels pointer is NULL");
+    if (phase == 0 || (phase & ~3u)) return fail(ctx, PSN_ERR_ARG, "phase must be PSN_COUNT, PSN_EMIT or both");
+    if (!ws || ws_bytes < L.total) return fail(ctx, PSN_ERR_ARG, "workspace too small: need %zu bytes", L.total);
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int eb = (int)vol->dtype;
+    const bool vec = (L.M % 4 == 0) && ((reinterpret_cast<uintptr_t>(vol->labels) & 15u) == 0);
+    LabelSet ls;
+    bool anz = true;
+    s = prepare_labels(ctx, vol, labels, ws, L, st, &ls, &anz);
+    if (s != PSN_OK) return s;
+    const void *slab0 = vol->labels;   // pointer to slice z_lo
+
+    if (phase & PSN_COUNT) {
+        if (cudaMemsetAsync(at<char>(ws, L.hdr), 0, L.cntP - L.hdr, st) != cudaSuccess) return cuda_check(ctx, "memset");
+        const int64_t nXT = (L.W4 + 7) / 8;
+        const int64_t WX = std::min<int64_t>(L.W4, 8);
+        const int tj = eb == 1 ? tj_of<uint8_t>() : (eb == 2 ? tj_of<uint16_t>() : tj_of<uint32_t>());
+        const int64_t nJB = (L.N - 1 + tj - 1) / tj;
+        const int64_t nLay = L.kB - L.kA;
+        const int64_t target_warps = (int64_t)ctx->sms * 48;
+        int64_t nZC = std::max<int64_t>(1, (target_warps + nXT * nJB * WX - 1) / (nXT * nJB * WX));
+        nZC = std::min(nZC, nLay);
+        const int64_t KZ = (nLay + nZC - 1) / nZC;
+        nZC = (nLay + KZ - 1) / KZ;
+        CountArgs ca;
+        ca.labels = slab0; ca.M = L.M; ca.N = L.N; ca.O = L.O; ca.z_lo = vol->z_lo;
+        ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W4 = L.W4;
+        ca.nXT = nXT; ca.nJB = nJB; ca.KZ = KZ;
+        ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
+        ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask);
+        ca.ls = ls; ca.multi_xt = nXT > 1 ? 1 : 0;
+        const int64_t gridR = std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8);
+        if (ca.multi_xt) {
+            k_init_multixt<<<(unsigned)gridR, 256, 0, st>>>(ca.cntP, ca.cntQ, ca.cntS, ca.trim, L.R);
+            ++ctx->launches;
+        }
+        const int64_t blocks = nXT * nJB * nZC;
+        const int threads = (int)(32 * WX);
+        if (eb == 1) dispatch_count<uint8_t>(ca, anz, vec, blocks, threads, st);
+        else if (eb == 2) dispatch_count<uint16_t>(ca, anz, vec, blocks, threads, st);
+        else dispatch_count<uint32_t>(ca, anz, vec, blocks, threads, st);
+        ++ctx->launches;
+        if (ca.multi_xt) {
+            k_trim_fix<<<(unsigned)gridR, 256, 0, st>>>(ca.trim, ca.cntP, L.R);
+            ++ctx->launches;
+        }
+        ScanArgs sa;
+        sa.cntP = ca.cntP; sa.cntQ = ca.cntQ; sa.cntS = ca.cntS;
+        sa.offP = at<uint32_t>(ws, L.offP); sa.offQ = at<uint32_t>(ws, L.offQ); sa.offS = at<uint32_t>(ws, L.offS);
+        sa.R = L.R;
+        sa.own_row0 = (L.N - 1) * (vol->own_k0 - L.kA);
+        sa.own_row1 = (L.N - 1) * (vol->own_k1 - L.kA);
+        sa.tiles = at<TileStatus>(ws, L.tiles); sa.hdr = at<ScanHeader>(ws, L.hdr);
+        k_scan<<<(unsigned)L.nTiles, kScanThreads, 0, st>>>(sa);
+        ++ctx->launches;
+        if ((s = cuda_check(ctx, "count/scan launch")) != PSN_OK) return s;
+        ctx->counted_ws = ws;
+        signature(vol, ctx->counted_sig);
+        if (!(phase & PSN_EMIT)) return read_totals(ctx, vol, L, ws, mesh, st, nullptr);
+    } else {
+        int64_t sig[6];
+        signature(vol, sig);
+        if (ctx->counted_ws != ws || memcmp(sig, ctx->counted_sig, sizeof(sig)) != 0)
+            return fail(ctx, PSN_ERR_STATE, "PSN_EMIT needs a preceding PSN_COUNT of the same volume on this workspace");
+        if (mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points > mesh->cap_points ||
+            mesh->n_quads > mesh->cap_quads || mesh->n_stencil > mesh->cap_stencil)
+            return fail(ctx, PSN_ERR_CAPACITY, "capacity too small: need points %lld quads %lld stencil %lld",
+                        (long long)(mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points),
+                        (long long)mesh->n_quads, (long long)mesh->n_stencil);
+    }
+    // ---- EMIT
+    if (!mesh->points || !mesh->quads || !mesh->pairs || !mesh->stencil_offsets || !mesh->stencil_ids || !mesh->face_masks)
+        return fail(ctx, PSN_ERR_ARG, "mesh output pointers must be non-NULL");
+    if ((reinterpret_cast<uintptr_t>(mesh->quads) & 15u) || (reinterpret_cast<uintptr_t>(mesh->pairs) & 7u))
+        return fail(ctx, PSN_ERR_ARG, "quads must be 16-byte and pairs 8-byte aligned");
+    EmitArgs ea;
+    ea.labels = slab0; ea.M = L.M; ea.N = L.N; ea.O = L.O; ea.z_lo = vol->z_lo;
+    ea.kA = L.kA; ea.kB = L.kB; ea.own_k0 = vol->own_k0; ea.own_k1 = vol->own_k1; ea.W4 = L.W4; ea.R = L.R;
+    ea.cntP = at<uint32_t>(ws, L.cntP); ea.offP = at<uint32_t>(ws, L.offP);
+    ea.offQ = at<uint32_t>(ws, L.offQ); ea.offS = at<uint32_t>(ws, L.offS); ea.pmask = at<uint32_t>(ws, L.pmask);
+    ea.ls = ls;
+    for (int a = 0; a < 3; ++a) { ea.sp[a] = vol->spacing[a]; ea.org[a] = vol->origin[a]; }
+    ea.points = mesh->points; ea.quads = mesh->quads; ea.pairs = mesh->pairs;
+    ea.csr_off = mesh->stencil_offsets; ea.csr_ids = mesh->stencil_ids; ea.fmask = mesh->face_masks;
+    ea.cap_points = mesh->cap_points; ea.cap_quads = mesh->cap_quads; ea.cap_stencil = mesh->cap_stencil;
+    ea.first_point = (uint32_t)mesh->first_point; ea.first_quad = (uint32_t)mesh->first_quad;
+    ea.first_stencil = (uint32_t)mesh->first_stencil;
+    ea.hdr = at<ScanHeader>(ws, L.hdr);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
+    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, vec, blocks, st);
+    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, vec, blocks, st);
+    else dispatch_emit<uint32_t>(ea, anz, vec, blocks, st);
+    ++ctx->launches;
+    return cuda_check(ctx, "emit launch");
+}
+
+psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, const void *ws, size_t ws_bytes,
+                           void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    Layout L;
+    psn_status s = layout(ctx, vol, &L);
+    if (s != PSN_OK) return s;
+    if (!mesh || !ws || ws_bytes < L.total) return fail(ctx, PSN_ERR_ARG, "bad mesh or workspace");
+    uint32_t es = 0;
+    s = read_totals(ctx, vol, L, ws, mesh, static_cast<cudaStream_t>(stream), &es);
+    if (s != PSN_OK) return s;
+    if (es) return fail(ctx, PSN_ERR_CAPACITY, "emission skipped: capacities too small");
+    return PSN_OK;
+}
+
+psn_status psn_smooth_workspace(int64_t n_points_window, size_t *bytes) {
+    if (!bytes || n_points_window < 0) return PSN_ERR_ARG;
+    *bytes = 2 * align_up(12 * (size_t)n_points_window);
+    return PSN_OK;
+}
+
+namespace {
+psn_status check_smooth_args(psn_ctx *ctx, const psn_mesh *mesh, float relaxation, float d) {
+    if (!mesh) return fail(ctx, PSN_ERR_ARG, "mesh is NULL");
+    if (!(relaxation >= 0.f && relaxation <= 1.f)) return fail(ctx, PSN_ERR_ARG, "relaxation must be in [0,1]");
+    if (!(d >= 0.f)) return fail(ctx, PSN_ERR_ARG, "constraint distance must be >= 0");
+    if (mesh->n_points < 0 || mesh->halo_lo_points < 0 || mesh->halo_hi_points < 0)
+        return fail(ctx, PSN_ERR_ARG, "negative point counts");
+    if (mesh->n_points > 0 && (!mesh->face_masks || !mesh->stencil_offsets || (!mesh->stencil_ids && mesh->n_stencil > 0)))
+        return fail(ctx, PSN_ERR_ARG, "mesh stencil arrays are NULL");
+    return PSN_OK;
+}
+
+SmoothArgs smooth_args(const psn_mesh *mesh, float lambda, float d) {
+    SmoothArgs a;
+    memset(&a, 0, sizeof(a));
+    a.fmask = mesh->face_masks; a.csr_off = mesh->stencil_offsets; a.csr_ids = mesh->stencil_ids;
+    a.points = mesh->points; a.n_own = mesh->n_points;
+    a.halo_lo = (uint32_t)mesh->halo_lo_points;
+    a.win_base = (uint32_t)(mesh->first_point - mesh->halo_lo_points);
+    a.first_stencil = (uint32_t)mesh->first_stencil;
+    a.lambda = lambda; a.d = d;
+    return a;
+}
+
+int64_t grid_for(psn_ctx *ctx, int64_t n) {
+    return std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 16));
+}
+}  // namespace
+
+psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, float *out, int32_t iterations,
+                      float relaxation, float constraint_distance, void *ws, size_t ws_bytes, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
+    if (s != PSN_OK) return s;
+    if (!vol) return fail(ctx, PSN_ERR_ARG, "volume is NULL");
+    if (iterations < 0) return fail(ctx, PSN_ERR_ARG, "iterations must be >= 0");
+    if (mesh->halo_lo_points || mesh->halo_hi_points)
+        return fail(ctx, PSN_ERR_ARG, "psn_smooth needs a whole volume; slabs use psn_smooth_step + halo exchange");
+    const int64_t nw = mesh->n_points;
+    size_t need = 0;
+    psn_smooth_workspace(nw, &need);
+    if (!out || !mesh->points || (iterations > 1 && (!ws || ws_bytes < need)))
+        return fail(ctx, PSN_ERR_ARG, "out/points NULL or workspace too small (need %zu)", need);
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nw == 0) return PSN_OK;
+    float *buf[2] = {static_cast<float *>(ws), ws ? reinterpret_cast<float *>(static_cast<char *>(ws) + need / 2) : nullptr};
+    const int64_t g = grid_for(ctx, nw);
+    if (iterations == 0) {
+        k_finalize<<<(unsigned)g, 256, 0, st>>>(nullptr, mesh->points, out, 0, nw, vol->spacing[0], vol->spacing[1],
+                                               vol->spacing[2], vol->origin[0], vol->origin[1], vol->origin[2]);
+        ++ctx->launches;
+        return cuda_check(ctx, "finalize launch");
+    }
+    SmoothArgs a = smooth_args(mesh, relaxation, constraint_distance);
+    for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
+    const float *src = nullptr;
+    for (int32_t t = 0; t < iterations; ++t) {
+        a.src = src;
+        const bool last = (t == iterations - 1);
+        a.dst = last ? nullptr : buf[t & 1];
+        a.world = last ? out : nullptr;
+        k_smooth<<<(unsigned)g, 256, 0, st>>>(a);
+        ++ctx->launches;
+        src = a.dst;
+    }
+    return cuda_check(ctx, "smooth launch");
+}
+
+psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const float *src, float *dst, float relaxation,
+                           float constraint_distance, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
+    if (s != PSN_OK) return s;
+    if (!dst) return fail(ctx, PSN_ERR_ARG, "dst is NULL");
+    if (mesh->n_points == 0) return PSN_OK;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    SmoothArgs a = smooth_args(mesh, relaxation, constraint_distance);
+    a.src = src; a.dst = dst; a.world = nullptr;
+    k_smooth<<<(unsigned)grid_for(ctx, mesh->n_points), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    ++ctx->launches;
+    return cuda_check(ctx, "smooth step launch");
+}
+
+psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const float *offsets,
+                               int64_t w0, int64_t w1, float *out, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    if (!vol || !mesh || !out || !mesh->points) return fail(ctx, PSN_ERR_ARG, "NULL argument");
+    const int64_t nw = mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points;
+    if (w0 < 0 || w1 > nw || w0 > w1) return fail(ctx, PSN_ERR_ARG, "window range out of bounds");
+    if (w0 == w1) return PSN_OK;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    k_finalize<<<(unsigned)grid_for(ctx, w1 - w0), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        offsets, mesh->points, out, w0, w1, vol->spacing[0], vol->spacing[1], vol->spacing[2], vol->origin[0],
+        vol->origin[1], vol->origin[2]);
+    ++ctx->launches;
+    return cuda_check(ctx, "finalize launch");
+}
+
+psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *points, psn_tri tri, uint32_t *tris,
+                           void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    if (!mesh || !tris || (mesh->n_quads > 0 && (!mesh->quads || !points)))
+        return fail(ctx, PSN_ERR_ARG, "NULL argument");
+    if (tri != PSN_TRI_FIXED_02 && tri != PSN_TRI_SHORTEST) return fail(ctx, PSN_ERR_ARG, "unknown triangulation");
+    if ((reinterpret_cast<uintptr_t>(mesh->quads) & 15u) || (reinterpret_cast<uintptr_t>(tris) & 7u))
+        return fail(ctx, PSN_ERR_ARG, "quads must be 16-byte and tris 8-byte aligned");
+    if (mesh->n_quads == 0) return PSN_OK;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    k_triangulate<<<(unsigned)grid_for(ctx, mesh->n_quads), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        mesh->quads, points, tris, mesh->n_quads, (uint32_t)(mesh->first_point - mesh->halo_lo_points),
+        tri == PSN_TRI_SHORTEST ? 1 : 0);
+    ++ctx->launches;
+    return cuda_check(ctx, "triangulate launch");
+}
+
+}  // extern "C"

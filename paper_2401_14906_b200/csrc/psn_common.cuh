@@ -1,0 +1,202 @@
+// psn_common.cuh -- device helpers shared by the PSN kernels (sm_100a).
+//
+// Data model: every lane owns a CHUNK of 4 consecutive
+// lattice points of a grid row, held as NW packed 32-bit words
+// (u8: 1 word, u16: 2 words, u32: 4 words).  A warp therefore covers 128
+// consecutive x positions.  Per-element boolean planes are kept in SPREAD
+// form: the most significant bit of each element slot is the flag, the other
+// bits are don't-care until masked with Pack<T>::MSB.
+//
+// Edge predicate (reading Q1): I(a,b) = cls(a) != cls(b).  With
+// all_nonzero (reading Q2) cls is injective on raw values, so I is a raw
+// inequality; for a general label set L each raw value is first mapped to a
+// CODE (v if v in L, else one fixed value z not in L), which is again
+// injective on classes.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace psn {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kBackground = 0xFFFFFFFFu;
+
+template <typename T> struct Pack;
+template <> struct Pack<uint8_t> {
+    static constexpr int NW = 1, EB = 8, EPW = 4;
+    static constexpr uint32_t LOW = 0x7F7F7F7Fu, MSB = 0x80808080u, EMASK = 0xFFu;
+};
+template <> struct Pack<uint16_t> {
+    static constexpr int NW = 2, EB = 16, EPW = 2;
+    static constexpr uint32_t LOW = 0x7FFF7FFFu, MSB = 0x80008000u, EMASK = 0xFFFFu;
+};
+template <> struct Pack<uint32_t> {
+    static constexpr int NW = 4, EB = 32, EPW = 1;
+    static constexpr uint32_t LOW = 0x7FFFFFFFu, MSB = 0x80000000u, EMASK = 0xFFFFFFFFu;
+};
+
+// Spread-form "elements differ": MSB of each element slot set iff a_e != b_e.
+// ((t & LOW) + LOW) carries into the MSB iff the low bits are non-zero; OR t
+// adds the MSB itself.  No carry crosses slots because LOW clears each MSB.
+template <typename T>
+__device__ __forceinline__ uint32_t neq(uint32_t a, uint32_t b) {
+    uint32_t t = a ^ b;
+    return ((t & Pack<T>::LOW) + Pack<T>::LOW) | t;
+}
+
+// Words of the chunk shifted by one element: element e of the result is
+// element e+1 of the chunk; the last slot takes the first element of `nxt`.
+template <typename T>
+__device__ __forceinline__ void shift1(const uint32_t (&w)[Pack<T>::NW], uint32_t nxt,
+                                       uint32_t (&h)[Pack<T>::NW]) {
+    constexpr int NW = Pack<T>::NW;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+        uint32_t hi = (q + 1 < NW) ? w[(q + 1) % NW] : nxt;
+        h[q] = __funnelshift_rc(w[q], hi, Pack<T>::EB);
+    }
+}
+
+// Flag bit of element e (0..3) of a spread plane.
+template <typename T>
+__device__ __forceinline__ uint32_t flag(const uint32_t (&p)[Pack<T>::NW], int e) {
+    constexpr int EPW = Pack<T>::EPW, EB = Pack<T>::EB;
+    return (p[e / EPW] >> (EB * (e % EPW) + EB - 1)) & 1u;
+}
+
+// Raw element e (0..3) of a packed chunk.
+template <typename T>
+__device__ __forceinline__ uint32_t elem(const uint32_t (&w)[Pack<T>::NW], int e) {
+    constexpr int EPW = Pack<T>::EPW, EB = Pack<T>::EB;
+    return (EB == 32) ? w[e] : ((w[e / EPW] >> (EB * (e % EPW))) & Pack<T>::EMASK);
+}
+
+// ---------------------------------------------------------------- loaders
+// Chunk of 4 elements starting at x0 (multiple of 4) of a row of M elements.
+// VEC: one aligned vector load when the chunk is complete (requires rows
+// aligned to 4*NW bytes, i.e. M % 4 == 0 and a 16-byte aligned base).
+// Elements >= M are zero-filled (they belong to no voxel).
+template <typename T, bool VEC>
+__device__ __forceinline__ void load_chunk(const T *__restrict__ row, int64_t x0, int64_t M,
+                                           uint32_t (&w)[Pack<T>::NW]) {
+    constexpr int NW = Pack<T>::NW;
+    if (VEC && x0 + 4 <= M) {
+        if constexpr (NW == 1) {
+            w[0] = __ldg(reinterpret_cast<const uint32_t *>(row + x0));
+        } else if constexpr (NW == 2) {
+            uint2 v = __ldg(reinterpret_cast<const uint2 *>(row + x0));
+            w[0] = v.x; w[1] = v.y;
+        } else {
+            uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + x0));
+            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        }
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < NW; ++q) w[q] = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        uint32_t v = (x0 + e < M) ? (uint32_t)__ldg(row + x0 + e) : 0u;
+        w[e / Pack<T>::EPW] |= v << (Pack<T>::EB * (e % Pack<T>::EPW) % 32);
+    }
+}
+
+// First packed word of the chunk starting at x0 (used for the element after a
+// lane's chunk when it lives in another warp).
+template <typename T, bool VEC>
+__device__ __forceinline__ uint32_t load_word(const T *__restrict__ row, int64_t x0, int64_t M) {
+    constexpr int EPW = Pack<T>::EPW;
+    if (VEC && x0 + EPW <= M) return __ldg(reinterpret_cast<const uint32_t *>(row + x0));
+    uint32_t w = 0;
+#pragma unroll
+    for (int e = 0; e < EPW; ++e) {
+        uint32_t v = (x0 + e < M) ? (uint32_t)__ldg(row + x0 + e) : 0u;
+        w |= v << (Pack<T>::EB * e % 32);
+    }
+    return w;
+}
+
+// ---------------------------------------------------------------- classification
+// General label sets (not all_nonzero): u8/u16 use a bitset of 2^bits in shared
+// memory, u32 a sorted list in global memory.  code(v) = v if v in L else z.
+struct LabelSet {
+    const uint32_t *bits;   // bitset (u8/u16) -- shared memory copy
+    const uint32_t *list;   // sorted unique values (u32)
+    int64_t n_list;
+    uint32_t z;             // a value not in L (code of every background value)
+    int identity;           // every value of the dtype is in L: code(v) = v
+};
+
+__device__ __forceinline__ bool in_list(const uint32_t *__restrict__ L, int64_t n, uint32_t v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        uint32_t x = __ldg(L + mid);
+        if (x == v) return true;
+        if (x < v) lo = mid + 1; else hi = mid;
+    }
+    return false;
+}
+
+template <typename T>
+__device__ __forceinline__ bool in_L(const LabelSet &ls, uint32_t v) {
+    if (sizeof(T) == 4) return in_list(ls.list, ls.n_list, v);
+    return (ls.bits[v >> 5] >> (v & 31)) & 1u;
+}
+
+template <typename T>
+__device__ __forceinline__ void remap(const LabelSet &ls, uint32_t (&w)[Pack<T>::NW]) {
+    if (ls.identity) return;
+    constexpr int NW = Pack<T>::NW, EPW = Pack<T>::EPW, EB = Pack<T>::EB;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+        uint32_t out = 0;
+#pragma unroll
+        for (int e = 0; e < EPW; ++e) {
+            uint32_t v = (EB == 32) ? w[q] : ((w[q] >> (EB * e)) & Pack<T>::EMASK);
+            uint32_t c = in_L<T>(ls, v) ? v : ls.z;
+            out |= (EB == 32) ? c : (c << (EB * e));
+        }
+        w[q] = out;
+    }
+}
+
+// Remap the elements of one packed word (the `next` word loaded directly).
+template <typename T>
+__device__ __forceinline__ uint32_t remap1(const LabelSet &ls, uint32_t w) {
+    if (ls.identity) return w;
+    constexpr int EPW = Pack<T>::EPW, EB = Pack<T>::EB;
+    uint32_t out = 0;
+#pragma unroll
+    for (int e = 0; e < EPW; ++e) {
+        uint32_t v = (EB == 32) ? w : ((w >> (EB * e)) & Pack<T>::EMASK);
+        uint32_t c = in_L<T>(ls, v) ? v : ls.z;
+        out |= (EB == 32) ? c : (c << (EB * e));
+    }
+    return out;
+}
+
+// Class of a coded element for the two-tuple (reading Q3): background -> sentinel.
+template <typename T, bool ANZ>
+__device__ __forceinline__ uint32_t cls_of_code(const LabelSet &ls, uint32_t code) {
+    if (ANZ) return code == 0 ? kBackground : code;
+    if (ls.identity) return code;
+    return code == ls.z ? kBackground : code;
+}
+
+// ---------------------------------------------------------------- memory-order helpers
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace psn

@@ -1,0 +1,323 @@
+"""Thin ctypes binding of the C ABI in include/psn.h (argument marshalling only).
+
+Every step of the hot path runs in libpsn.so's sm_100a kernels; this module
+only converts torch tensors to pointers and sizes, allocates output tensors
+with the exact sizes the COUNT phase reports ("memory is
+precisely allocated"), and raises on any non-OK status.  There is no CPU
+fallback: if the extension or a CUDA device is missing, it raises.
+
+Names follow include/psn.h: psn_extract / psn_smooth / psn_triangulate.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpsn.so")
+
+PSN_OK, PSN_ERR_ARG, PSN_ERR_LABELS, PSN_ERR_OVERFLOW, PSN_ERR_CAPACITY, PSN_ERR_STATE, PSN_ERR_CUDA = range(7)
+PSN_COUNT, PSN_EMIT = 1, 2
+PSN_TRI_FIXED_02, PSN_TRI_SHORTEST = 0, 1
+BACKGROUND = 0xFFFFFFFF
+
+_DTYPES = {torch.uint8: 1, torch.uint16: 2, torch.uint32: 4}
+
+
+class PSNError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "PSN_OK", 1: "PSN_ERR_ARG", 2: "PSN_ERR_LABELS", 3: "PSN_ERR_OVERFLOW",
+           4: "PSN_ERR_CAPACITY", 5: "PSN_ERR_STATE", 6: "PSN_ERR_CUDA"}
+
+
+class Volume(ctypes.Structure):
+    _fields_ = [("labels", ctypes.c_void_p), ("dtype", ctypes.c_int), ("dims", ctypes.c_int64 * 3),
+                ("spacing", ctypes.c_double * 3), ("origin", ctypes.c_double * 3),
+                ("z_lo", ctypes.c_int64), ("z_hi", ctypes.c_int64),
+                ("own_k0", ctypes.c_int64), ("own_k1", ctypes.c_int64)]
+
+
+class Labels(ctypes.Structure):
+    _fields_ = [("values", ctypes.POINTER(ctypes.c_uint32)), ("count", ctypes.c_int64), ("all_nonzero", ctypes.c_int)]
+
+
+class MeshC(ctypes.Structure):
+    _fields_ = [("points", ctypes.c_void_p), ("quads", ctypes.c_void_p), ("pairs", ctypes.c_void_p),
+                ("stencil_offsets", ctypes.c_void_p), ("stencil_ids", ctypes.c_void_p),
+                ("face_masks", ctypes.c_void_p),
+                ("cap_points", ctypes.c_int64), ("cap_quads", ctypes.c_int64), ("cap_stencil", ctypes.c_int64),
+                ("n_points", ctypes.c_int64), ("n_quads", ctypes.c_int64), ("n_stencil", ctypes.c_int64),
+                ("halo_lo_points", ctypes.c_int64), ("halo_hi_points", ctypes.c_int64),
+                ("first_point", ctypes.c_int64), ("first_quad", ctypes.c_int64), ("first_stencil", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpsn.so (build it with __graft_entry__.build()); raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libpsn.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64 = ctypes.c_void_p, ctypes.c_int64
+        L.psn_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+        L.psn_ctx_create.restype = ctypes.c_int
+        L.psn_ctx_destroy.argtypes = [vp]
+        L.psn_ctx_destroy.restype = None
+        L.psn_last_error.argtypes = [vp]
+        L.psn_last_error.restype = ctypes.c_char_p
+        L.psn_status_string.argtypes = [ctypes.c_int]
+        L.psn_status_string.restype = ctypes.c_char_p
+        L.psn_extract_workspace.argtypes = [ctypes.POINTER(Volume), ctypes.POINTER(ctypes.c_size_t)]
+        L.psn_extract_workspace.restype = ctypes.c_int
+        L.psn_extract.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(Labels), ctypes.POINTER(MeshC),
+                                  ctypes.c_uint, vp, ctypes.c_size_t, vp]
+        L.psn_extract.restype = ctypes.c_int
+        L.psn_mesh_totals.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
+        L.psn_mesh_totals.restype = ctypes.c_int
+        L.psn_smooth_workspace.argtypes = [i64, ctypes.POINTER(ctypes.c_size_t)]
+        L.psn_smooth_workspace.restype = ctypes.c_int
+        L.psn_smooth.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_int32,
+                                 ctypes.c_float, ctypes.c_float, vp, ctypes.c_size_t, vp]
+        L.psn_smooth.restype = ctypes.c_int
+        L.psn_smooth_step.argtypes = [vp, ctypes.POINTER(MeshC), vp, vp, ctypes.c_float, ctypes.c_float, vp]
+        L.psn_smooth_step.restype = ctypes.c_int
+        L.psn_smooth_finalize.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, i64, i64, vp, vp]
+        L.psn_smooth_finalize.restype = ctypes.c_int
+        L.psn_triangulate.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_int, vp, vp]
+        L.psn_triangulate.restype = ctypes.c_int
+        L.psn_launch_count.argtypes = [vp]
+        L.psn_launch_count.restype = i64
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
+            "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
+            "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count"]
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class Mesh:
+    """Device mesh (window-indexed points, own-point stencils, own quads)."""
+    points: torch.Tensor          # float32 [halo_lo + P + halo_hi, 3]
+    quads: torch.Tensor           # uint32 [Q, 4] (stored as int32 view)
+    pairs: torch.Tensor           # uint32 [Q, 2]
+    stencil_offsets: torch.Tensor  # uint32 [P + 1]
+    stencil_ids: torch.Tensor     # uint32 [S]
+    face_masks: torch.Tensor      # uint8 [P]
+    c: MeshC = field(default_factory=MeshC)
+
+    @property
+    def n_points(self):
+        return self.c.n_points
+
+    @property
+    def n_quads(self):
+        return self.c.n_quads
+
+    @property
+    def n_stencil(self):
+        return self.c.n_stencil
+
+    @property
+    def n_window(self):
+        return self.c.halo_lo_points + self.c.n_points + self.c.halo_hi_points
+
+
+class PSN:
+    """One context per device (psn_ctx)."""
+
+    def __init__(self, device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("PSN needs a CUDA device (no CPU fallback)")
+        self.L = lib()
+        self.device = device
+        h = ctypes.c_void_p()
+        rc = self.L.psn_ctx_create(device, ctypes.byref(h))
+        if rc != PSN_OK:
+            raise PSNError(rc, "psn_ctx_create failed")
+        self.h = h
+        self._ws = {}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.L.psn_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != PSN_OK:
+            raise PSNError(rc, self.L.psn_last_error(self.h).decode())
+
+    @property
+    def launches(self):
+        return self.L.psn_launch_count(self.h)
+
+    # ------------------------------------------------------------------ volume / labels
+    @staticmethod
+    def volume(labels: torch.Tensor, dims=None, spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 0.0),
+               z_lo: int = 0, own=None) -> Volume:
+        if labels.dtype not in _DTYPES or not labels.is_cuda or not labels.is_contiguous():
+            raise ValueError("labels must be a contiguous CUDA uint8/uint16/uint32 tensor (z, y, x)")
+        Z, N, M = labels.shape
+        if dims is None:
+            dims = (M, N, Z)
+        v = Volume()
+        v.labels = labels.data_ptr()
+        v.dtype = _DTYPES[labels.dtype]
+        for a in range(3):
+            v.dims[a] = int(dims[a]); v.spacing[a] = float(spacing[a]); v.origin[a] = float(origin[a])
+        v.z_lo, v.z_hi = z_lo, z_lo + Z
+        k0, k1 = own if own is not None else (0, dims[2] - 1)
+        v.own_k0, v.own_k1 = int(k0), int(k1)
+        return v
+
+    @staticmethod
+    def labels(label_set=None):
+        lab = Labels()
+        if label_set is None:
+            lab.all_nonzero = 1
+            lab.count = 0
+            lab._keep = None
+        else:
+            vals = list(label_set)
+            arr = (ctypes.c_uint32 * max(len(vals), 1))(*vals)
+            lab.values = ctypes.cast(arr, ctypes.POINTER(ctypes.c_uint32))
+            lab.count = len(vals)
+            lab.all_nonzero = 0
+            lab._keep = arr
+        return lab
+
+    def workspace(self, vol: Volume) -> torch.Tensor:
+        n = ctypes.c_size_t()
+        rc = self.L.psn_extract_workspace(ctypes.byref(vol), ctypes.byref(n))
+        self._check(rc)
+        return torch.empty(n.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    # ------------------------------------------------------------------ extraction
+    def count(self, vol: Volume, labels: Labels, ws: torch.Tensor, stream=None) -> MeshC:
+        """psn_extract(PSN_COUNT): totals (one stream synchronisation)."""
+        m = MeshC()
+        rc = self.L.psn_extract(self.h, ctypes.byref(vol), ctypes.byref(labels), ctypes.byref(m), PSN_COUNT,
+                                _ptr(ws), ws.numel(), _stream(stream))
+        self._check(rc)
+        return m
+
+    def alloc_mesh(self, n_window, n_points, n_quads, n_stencil) -> Mesh:
+        dev = f"cuda:{self.device}"
+        return Mesh(points=torch.empty((max(n_window, 1), 3), dtype=torch.float32, device=dev),
+                    quads=torch.empty((max(n_quads, 1), 4), dtype=torch.int32, device=dev),
+                    pairs=torch.empty((max(n_quads, 1), 2), dtype=torch.int32, device=dev),
+                    stencil_offsets=torch.empty(n_points + 1, dtype=torch.int32, device=dev),
+                    stencil_ids=torch.empty(max(n_stencil, 1), dtype=torch.int32, device=dev),
+                    face_masks=torch.empty(max(n_points, 1), dtype=torch.uint8, device=dev))
+
+    def _fill(self, mesh: Mesh, c: MeshC, first=(0, 0, 0)):
+        c.points = mesh.points.data_ptr(); c.quads = mesh.quads.data_ptr(); c.pairs = mesh.pairs.data_ptr()
+        c.stencil_offsets = mesh.stencil_offsets.data_ptr(); c.stencil_ids = mesh.stencil_ids.data_ptr()
+        c.face_masks = mesh.face_masks.data_ptr()
+        c.cap_points = mesh.points.shape[0]; c.cap_quads = mesh.quads.shape[0]; c.cap_stencil = mesh.stencil_ids.shape[0]
+        c.first_point, c.first_quad, c.first_stencil = (int(x) for x in first)
+        mesh.c = c
+
+    def emit(self, vol: Volume, labels: Labels, ws: torch.Tensor, counted: MeshC, first=(0, 0, 0),
+             mesh: Mesh | None = None, stream=None) -> Mesh:
+        """psn_extract(PSN_EMIT) into exactly allocated arrays."""
+        if mesh is None:
+            mesh = self.alloc_mesh(counted.halo_lo_points + counted.n_points + counted.halo_hi_points,
+                                   counted.n_points, counted.n_quads, counted.n_stencil)
+        c = MeshC.from_buffer_copy(counted)
+        self._fill(mesh, c, first)
+        rc = self.L.psn_extract(self.h, ctypes.byref(vol), ctypes.byref(labels), ctypes.byref(mesh.c), PSN_EMIT,
+                                _ptr(ws), ws.numel(), _stream(stream))
+        self._check(rc)
+        return mesh
+
+    def extract(self, vol: Volume, label_set=None, ws=None, stream=None) -> Mesh:
+        """Two-phase extraction: COUNT (exact totals) -> allocate -> EMIT."""
+        labels = self.labels(label_set)
+        if ws is None:
+            ws = self.workspace(vol)
+        counted = self.count(vol, labels, ws, stream)
+        mesh = self.emit(vol, labels, ws, counted, stream=stream)
+        mesh.ws = ws
+        return mesh
+
+    def extract_into(self, vol: Volume, labels: Labels, ws: torch.Tensor, mesh: Mesh, stream=None) -> None:
+        """Steady state: PSN_COUNT|PSN_EMIT with preallocated capacities, no host sync."""
+        c = MeshC()
+        self._fill(mesh, c)
+        rc = self.L.psn_extract(self.h, ctypes.byref(vol), ctypes.byref(labels), ctypes.byref(mesh.c),
+                                PSN_COUNT | PSN_EMIT, _ptr(ws), ws.numel(), _stream(stream))
+        self._check(rc)
+
+    def totals(self, vol: Volume, ws: torch.Tensor, mesh: Mesh, stream=None) -> Mesh:
+        rc = self.L.psn_mesh_totals(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(ws), ws.numel(),
+                                    _stream(stream))
+        self._check(rc)
+        return mesh
+
+    # ------------------------------------------------------------------ smoothing / triangulation
+    def smooth_workspace(self, n_window) -> torch.Tensor:
+        n = ctypes.c_size_t()
+        self._check(self.L.psn_smooth_workspace(int(n_window), ctypes.byref(n)))
+        return torch.empty(max(n.value, 1), dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def smooth(self, vol: Volume, mesh: Mesh, iterations: int, relaxation: float, constraint: float,
+               out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((max(mesh.n_window, 1), 3), dtype=torch.float32, device=mesh.points.device)
+        if ws is None:
+            ws = self.smooth_workspace(mesh.n_window)
+        rc = self.L.psn_smooth(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(out), int(iterations),
+                               float(relaxation), float(constraint), _ptr(ws), ws.numel(), _stream(stream))
+        self._check(rc)
+        return out
+
+    def smooth_step(self, mesh: Mesh, src: torch.Tensor | None, dst: torch.Tensor, relaxation: float,
+                    constraint: float, stream=None):
+        rc = self.L.psn_smooth_step(self.h, ctypes.byref(mesh.c), _ptr(src), _ptr(dst), float(relaxation),
+                                    float(constraint), _stream(stream))
+        self._check(rc)
+
+    def smooth_finalize(self, vol: Volume, mesh: Mesh, offsets: torch.Tensor | None, out: torch.Tensor,
+                        w0: int = 0, w1: int | None = None, stream=None):
+        w1 = mesh.n_window if w1 is None else w1
+        rc = self.L.psn_smooth_finalize(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(offsets), int(w0),
+                                        int(w1), _ptr(out), _stream(stream))
+        self._check(rc)
+        return out
+
+    def triangulate(self, mesh: Mesh, points: torch.Tensor, strategy: int = PSN_TRI_SHORTEST,
+                    out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((max(2 * mesh.n_quads, 1), 3), dtype=torch.int32, device=mesh.points.device)
+        rc = self.L.psn_triangulate(self.h, ctypes.byref(mesh.c), _ptr(points), int(strategy), _ptr(out),
+                                    _stream(stream))
+        self._check(rc)
+        return out
+
+
+def to_numpy_u32(t: torch.Tensor, n_rows: int):
+    """Device int32 view -> host numpy uint32 (first n_rows rows)."""
+    return t[:n_rows].cpu().numpy().view("uint32")

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element, on the same seeded inputs.  Extraction outputs must be bit-exact
+(points, quads, pairs, CSR offsets/ids, face masks); smoothed coordinates
+within 1e-4 x spacing per axis (BASELINE.json north_star); triangles
+bit-exact against host triangulation of the GPU's own fp32 points (C-8 i)."""
+import numpy as np
+import pytest
+import torch
+
+import gpu_util as gu
+import oracle
+import psn_gen
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4   # x spacing, per axis (north_star)
+
+
+def _corpus(rng, n, max_dim=40):
+    out = []
+    for t in range(n):
+        dims = [int(rng.integers(2, max_dim + 1)) for _ in range(3)]
+        if t % 7 == 0:
+            dims[0] = int(rng.choice([129, 131, 257, 130]))   # several warps, ragged last chunk
+        M, N, O = dims
+        dtype = [np.uint8, np.uint16, np.uint32][t % 3]
+        kind = t % 4
+        if kind == 0:
+            a = rng.integers(0, 4, size=(O, N, M))
+        elif kind == 1:
+            z, y, x = np.meshgrid(np.arange(O), np.arange(N), np.arange(M), indexing="ij")
+            c = rng.uniform(0, 1, 3) * np.array([M, N, O])
+            r = rng.uniform(1, max(2, min(dims) / 2))
+            a = ((x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2 <= r * r).astype(np.int64) * int(rng.integers(1, 200))
+        elif kind == 2:
+            a = np.zeros((O, N, M), np.int64)
+            a[1:-1, 1:-1, 1:-1] = rng.integers(0, 3, size=(max(O - 2, 0), max(N - 2, 0), max(M - 2, 0)))
+        else:
+            z, y, x = np.meshgrid(np.arange(O), np.arange(N), np.arange(M), indexing="ij")
+            a = (x // int(rng.integers(1, 9)) + 3 * (y // int(rng.integers(1, 9))) + 5 * (z // int(rng.integers(1, 9)))) % 6
+        a = a.astype(dtype)
+        if dtype == np.uint32 and t % 2:
+            a = a * np.uint32(1000003)
+        label_set = None
+        if t % 5 == 2:
+            vals = np.unique(a).tolist()
+            label_set = sorted(set(rng.choice(vals, size=max(1, len(vals) // 2)).tolist()) | {0})
+        elif t % 5 == 4:
+            vals = np.unique(a).tolist()
+            label_set = sorted(set(rng.choice(vals, size=max(1, (len(vals) + 1) // 2)).tolist()))
+        out.append((a, label_set))
+    return out
+
+
+def _check_volume(a, label_set=None, spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 0.0), T=5):
+    p, vol, mesh, dev = gu.gpu_extract(a, spacing, origin, label_set)
+    om = oracle.extract(oracle.as_volume(a, spacing, origin, label_set))
+    g = gu.mesh_np(mesh)
+    assert (mesh.n_points, mesh.n_quads, mesh.n_stencil) == (om.n_points, om.n_quads, om.n_stencil)
+    gu.assert_mesh_equal(g, om)
+    if om.n_points:
+        pts = p.smooth(vol, mesh, T, 0.5, 0.5)
+        ref = oracle.smooth(om, spacing, T, 0.5, 0.5)
+        err = np.abs(pts[:om.n_points].cpu().numpy().astype(np.float64) - ref) / np.array(spacing)
+        assert err.max() <= TOL, err.max()
+        # containment: |p - anchor| <= d*s + ulp32 of the fp32 output (its one rounding)
+        gp = pts[:om.n_points].cpu().numpy()
+        dev_ = np.abs(gp.astype(np.float64) - om.anchors)
+        ulp = np.spacing(np.maximum(np.abs(om.points), np.abs(gp)).astype(np.float32)).astype(np.float64)
+        assert np.all(dev_ <= 0.5 * np.array(spacing) + ulp)
+        if om.n_quads:
+            tris = p.triangulate(mesh, pts)
+            host = oracle.triangulate(om.quads, pts[:om.n_points].cpu().numpy())
+            np.testing.assert_array_equal(gu.u32(tris, 2 * om.n_quads), host)
+    return mesh
+
+
+def test_random_corpus_bit_exact():
+    rng = np.random.default_rng(20240126)
+    for a, ls in _corpus(rng, 120):
+        _check_volume(a, ls, spacing=(0.8, 1.0, 1.5), origin=(-3.0, 2.0, 10.0))
+
+
+def test_two_by_two_by_two_exhaustive():
+    """All 2^8 binary and 3^8 ternary 2x2x2 volumes in one batch each (as slabs of one volume
+    would mix them; here each is its own call through the ABI)."""
+    p = gu.psn()
+    for nval in (2, 3):
+        import itertools
+        for vals in itertools.product(range(nval), repeat=8):
+            a = np.array(vals, np.uint8).reshape(2, 2, 2)
+            _, vol, mesh, _ = gu.gpu_extract(a)
+            om = oracle.extract(oracle.as_volume(a))
+            assert (mesh.n_points, mesh.n_quads, mesh.n_stencil) == (om.n_points, om.n_quads, om.n_stencil)
+            if om.n_points:
+                gu.assert_mesh_equal(gu.mesh_np(mesh), om)
+    del p
+
+
+def test_iid_contains_every_2x2x2_pattern():
+    """Large iid volumes contain every 2x2x2 pattern thousands of times."""
+    rng = np.random.default_rng(5)
+    for dtype, M in ((np.uint8, 96), (np.uint16, 100), (np.uint32, 64)):
+        a = rng.integers(0, 3, size=(40, 37, M)).astype(dtype)
+        _check_volume(a, T=10)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_config_full(name):
+    spec = psn_gen.config(name)
+    dev = psn_gen.generate_device(spec)
+    host = psn_gen.generate_host(spec)
+    np.testing.assert_array_equal(dev.cpu().numpy(), host)
+    T, lam, d = psn_gen.SMOOTHING[name]
+    sp = tuple(spec.spacing)
+    p = gu.psn()
+    vol = p.volume(dev, spacing=sp)
+    mesh = p.extract(vol)
+    om = oracle.extract(oracle.as_volume(host, sp))
+    gu.assert_mesh_equal(gu.mesh_np(mesh), om)
+    pts = p.smooth(vol, mesh, T, lam, d)
+    ref = oracle.smooth(om, sp, T, lam, d)
+    gp = pts[:om.n_points].cpu().numpy()
+    err = np.abs(gp.astype(np.float64) - ref) / np.array(sp)
+    assert err.max() <= TOL, err.max()
+    tris = p.triangulate(mesh, pts)
+    np.testing.assert_array_equal(gu.u32(tris, 2 * om.n_quads), oracle.triangulate(om.quads, gp))
+    # C-8 (ii): against the fp64 oracle, differences only on near-ties
+    tref = oracle.triangulate(om.quads, ref.astype(np.float32))
+    diff = np.nonzero((gu.u32(tris, 2 * om.n_quads) != tref).any(1))[0] // 2
+    tau = TOL * max(sp)
+    for q in np.unique(diff):
+        v = om.quads[q]
+        d02 = np.linalg.norm(ref[v[2]] - ref[v[0]]); d13 = np.linalg.norm(ref[v[3]] - ref[v[1]])
+        assert abs(d02 ** 2 - d13 ** 2) <= 4 * np.sqrt(3) * tau * (d02 + d13) + 24 * tau ** 2
+
+
+def test_fused_count_emit_matches_two_phase():
+    spec = psn_gen.config("c2")
+    dev = psn_gen.generate_device(spec)
+    p = gu.psn()
+    vol = p.volume(dev)
+    ref = p.extract(vol)
+    g0 = gu.mesh_np(ref)
+    mesh = p.alloc_mesh(ref.n_window, ref.n_points, ref.n_quads, ref.n_stencil)
+    ws = p.workspace(vol)
+    lab = p.labels(None)
+    for _ in range(2):
+        p.extract_into(vol, lab, ws, mesh)
+        p.totals(vol, ws, mesh)
+        g = gu.mesh_np(mesh)
+        for k in g0:
+            np.testing.assert_array_equal(g[k], g0[k])
+    # too small capacity: the fused path skips emission and reports it
+    small = p.alloc_mesh(ref.n_window - 1, ref.n_points, ref.n_quads, ref.n_stencil)
+    p.extract_into(vol, lab, ws, small)
+    from paper_2401_14906_b200.psn import PSNError, PSN_ERR_CAPACITY
+    with pytest.raises(PSNError) as e:
+        p.totals(vol, ws, small)
+    assert e.value.status == PSN_ERR_CAPACITY
+
+
+def test_deterministic_repeats():
+    rng = np.random.default_rng(9)
+    a = rng.integers(0, 4, size=(30, 33, 70)).astype(np.uint16)
+    outs = [gu.mesh_np(gu.gpu_extract(a)[2]) for _ in range(3)]
+    for o in outs[1:]:
+        for k in o:
+            np.testing.assert_array_equal(o[k], outs[0][k])
+
+
+def test_degenerate_and_errors():
+    from paper_2401_14906_b200.psn import PSNError, PSN_ERR_ARG, PSN_ERR_LABELS
+    p = gu.psn()
+    for a in (np.zeros((8, 8, 8), np.uint8), np.full((8, 8, 8), 7, np.uint16), np.zeros((2, 2, 2), np.uint8)):
+        _, _, mesh, _ = gu.gpu_extract(a)
+        assert (mesh.n_points, mesh.n_quads, mesh.n_stencil) == (0, 0, 0)
+        assert int(mesh.stencil_offsets[0]) == 0
+    dev = torch.zeros((1, 4, 4), dtype=torch.uint8, device="cuda")
+    with pytest.raises(PSNError) as e:
+        p.extract(p.volume(dev))          # O = 1 < 2
+    assert e.value.status == PSN_ERR_ARG
+    dev = torch.zeros((4, 4, 4), dtype=torch.uint8, device="cuda")
+    with pytest.raises(PSNError) as e:
+        p.extract(p.volume(dev), label_set=[])
+    assert e.value.status == PSN_ERR_LABELS
+    with pytest.raises(PSNError) as e:
+        p.extract(p.volume(dev), label_set=[0xFFFFFFFF])
+    assert e.value.status == PSN_ERR_LABELS
+    with pytest.raises(PSNError) as e:
+        p.extract(p.volume(dev, spacing=(1.0, 0.0, 1.0)))
+    assert e.value.status == PSN_ERR_ARG
+    _, vol, mesh, _ = gu.gpu_extract(np.pad(np.ones((2, 2, 2), np.uint8), 2))
+    with pytest.raises(PSNError) as e:
+        p.smooth(vol, mesh, 3, 1.5, 0.5)
+    assert e.value.status == PSN_ERR_ARG
+
+
+def test_smoothing_zero_iterations_is_anchors():
+    rng = np.random.default_rng(2)
+    a = rng.integers(0, 3, size=(12, 13, 17)).astype(np.uint8)
+    p, vol, mesh, _ = gu.gpu_extract(a, spacing=(0.8, 0.8, 1.5), origin=(5.0, -1.0, 0.25))
+    pts = p.smooth(vol, mesh, 0, 0.5, 0.5)
+    np.testing.assert_array_equal(pts[:mesh.n_points].cpu().numpy(), mesh.points[:mesh.n_points].cpu().numpy())
+    pts = p.smooth(vol, mesh, 4, 0.0, 0.5)
+    np.testing.assert_array_equal(pts[:mesh.n_points].cpu().numpy(), mesh.points[:mesh.n_points].cpu().numpy())
+
+
+def test_wide_rows_multi_xtile():
+    """M > 1024 splits rows over several CTAs (global-atomic row counters)."""
+    rng = np.random.default_rng(77)
+    a = rng.integers(0, 3, size=(4, 5, 1500)).astype(np.uint16)
+    _check_volume(a, T=3)
+    a = np.zeros((5, 6, 2100), np.uint8)
+    a[2, 2:4, 1000:1100] = 3
+    _check_volume(a, T=3)
