@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- PSN hot path on B200: extraction (k_count -> k_scan -> k_emit) +
+T-iteration constrained smoothing (k_smooth), timed with CUDA events.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl psn|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL): the c4 volume is
+z-slab partitioned (strong scaling, total work fixed), with the all-gather of
+per-rank totals (C1) and the per-iteration halo exchange (C2).
+
+One JSON line on rank 0.  `value` = label voxels of the whole volume pushed
+through one step (extraction + T smoothing iterations) per second; the
+`extract` / `smooth` sub-objects give the two halves of BASELINE.json's metric
+(voxels/s extracted, smoothed point-iterations/s) and their HBM roofline
+fractions.  `--impl reference` times the oracle (oracle/, plain C, 1 core) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "label voxels/s extracted + smoothed point-iters/s, % of HBM roofline, 1–8 GPU"
+WORKLOADS = {
+    "c1": "c1: 32^3 u16, 3 spheres; extract + 10 smoothing iterations (lambda 0.5, box 0.5 voxel)",
+    "c2": "c2: 256^3 u8, 20-seed Voronoi in an ellipsoid; extract + 25 smoothing iterations + shortest-diagonal triangulation",
+    "c3": "c3: 512x512x600 u16 torso-like, spacing 0.8x0.8x1.5, 101 labels; extract + 25 smoothing iterations",
+    "c4": "c4: 1024^3 u16 atlas-like (200 Voronoi labels in a ball + 300 inclusions); extract + 50 smoothing iterations, z-slab over N GPUs",
+    "c5a": "c5a: 512^3 u8 iid {0,1,2,3}; extract + 10 smoothing iterations",
+    "c5b": "c5b: 512^3 u8 single sphere r=16; extract + 10 smoothing iterations",
+}
+TRIANGULATE = {"c2"}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def profile_traffic(kernel: str, config: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d[config][kernel]
+        return float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons, util = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1])); util.append(float(f[6]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- byte model
+def algorithmic_bytes(V, b, P, Q, S):
+    """B_ext = V*b + 12P + 16Q + 8Q + 4(P+1) + 4S; B_sm/iter = 24P + 4(P+1) + 4S."""
+    b_ext = V * b + 12 * P + 24 * Q + 4 * (P + 1) + 4 * S
+    b_sm = 24 * P + 4 * (P + 1) + 4 * S
+    return b_ext, b_sm
+
+
+# --------------------------------------------------------------------------- oracle (CPU baseline / reference arm)
+def sample_window(O: int, n_layers: int):
+    """Central voxel layers [k0, k1) plus one frozen layer each side [wa, wb) and
+    the lattice slices [z_lo, z_hi) the oracle needs for them."""
+    n_layers = max(1, min(n_layers, O - 1))
+    k0 = max(0, min((O - 1) // 2 - n_layers // 2, O - 1 - n_layers))
+    k1 = k0 + n_layers
+    wa, wb = max(k0 - 1, 0), min(k1 + 1, O - 1)
+    z_lo, z_hi = max(wa - 1, 0), min(wb + 1, O - 1) + 1
+    return n_layers, k0, k1, wa, wb, z_lo, z_hi
+
+
+def oracle_sample(cfg: str, n_layers: int, labels_host=None):
+    """Time the oracle (plain C, single thread) on voxel layers [k0, k0+n_layers) of the
+    config: extraction + T fp64 smoothing iterations.  The extracted window carries one
+    frozen voxel layer on each interior side so every stencil id stays inside it.
+    Returns (seconds, voxels, (k0, k1), labels_host)."""
+    import numpy as np
+
+    import oracle
+    import psn_gen
+    spec = psn_gen.config(cfg)
+    M, N, O = spec.M, spec.N, spec.O
+    T, lam, d = psn_gen.SMOOTHING[cfg]
+    n_layers, k0, k1, wa, wb, z_lo, z_hi = sample_window(O, n_layers)
+    if callable(labels_host):
+        labels_host = labels_host(z_lo, z_hi)
+    if labels_host is None:
+        labels_host = psn_gen.generate_host(spec, z_lo, z_hi)
+    vol = oracle.Volume(np.ascontiguousarray(labels_host), (M, N, O), z_lo, tuple(spec.spacing))
+    t0 = time.perf_counter()
+    mesh = oracle.extract(vol, wa, wb)
+    lay = mesh.voxel_idx[:, 2]
+    frozen = (((lay == wa) & (wa < k0)) | ((lay == wb - 1) & (wb > k1))).astype(np.uint8)
+    oracle.smooth(mesh, tuple(spec.spacing), T, lam, d, frozen=frozen)
+    dt = time.perf_counter() - t0
+    return dt, M * N * n_layers, (k0, k1), labels_host
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    cfg = args.config
+    import psn_gen
+    spec = psn_gen.config(cfg)
+    M, N = spec.M, spec.N
+    # bounded sample per step: ~2-4 s of single-core oracle work
+    n_layers = max(1, int(round(args.ref_voxels / (M * N))))
+    labels = None
+    times = []
+    for s in range(args.warmup + args.steps):
+        dt, vox, (k0, k1), labels = oracle_sample(cfg, n_layers, labels_host=labels)
+        if s >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    value = vox * len(times) / t
+    sample = f"{cfg} voxel layers [{k0},{k1}) ({vox} voxels): oracle extract + {psn_gen.SMOOTHING[cfg][0]}-iteration fp64 smoothing"
+    line = {"metric": METRIC, "value": value, "unit": "voxel/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u16/f64" if spec.elem_bytes == 2 else "u8/f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOADS[cfg], "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "voxel/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "voxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_psn(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import psn_gen
+    from paper_2401_14906_b200 import PSN
+    from paper_2401_14906_b200.psn import Pipeline, surface_nets_host
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = args.config
+    spec = psn_gen.config(cfg)
+    M, N, O = spec.M, spec.N, spec.O
+    b = spec.elem_bytes
+    V = M * N * O
+    T, lam, d = psn_gen.SMOOTHING[cfg]
+    sp = tuple(spec.spacing)
+    psn = PSN(local_rank)
+    stream = torch.cuda.current_stream()
+    tri = cfg in TRIANGULATE
+
+    if world == 1:
+        labels = psn_gen.generate_device(spec)
+        vol = psn.volume(labels, spacing=sp)
+        pipe = Pipeline(psn, vol, T, lam, d, triangulate=tri)
+        P, Q, S = pipe.counts
+        run_extract, run_smooth = pipe.extract, pipe.smooth
+    else:
+        from paper_2401_14906_b200.dist import SlabPipeline, partition, slab_slices
+        k0, k1 = partition(O - 1, world)[rank]
+        z_lo, z_hi = slab_slices(O, k0, k1)
+        labels = psn_gen.generate_device(spec, z_lo, z_hi)
+        pipe = SlabPipeline(psn, labels, (M, N, O), sp, (0.0, 0.0, 0.0), (k0, k1), T, lam, d)
+        tab = pipe.table
+        P, Q, S = (int(x) for x in tab[:, :3].sum(0))
+        run_extract = pipe.extract
+        run_smooth = pipe.smooth
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (W >= 3)
+    for _ in range(args.warmup):
+        run_extract()
+        run_smooth()
+    torch.cuda.synchronize()
+    if world == 1:
+        assert pipe.check(), "steady-state totals differ from the warm-up count"
+    launches = 0
+    if world == 1:
+        launches = sum(pipe.launches.values())
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for s in range(K):
+            ev[s][0].record(stream)
+            run_extract()
+            ev[s][1].record(stream)
+            run_smooth()
+            ev[s][2].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    t_ext = sum(e[0].elapsed_time(e[1]) for e in ev) / K    # ms per step
+    t_sm = sum(e[1].elapsed_time(e[2]) for e in ev) / K
+    t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / K
+    if world > 1:
+        tt = torch.tensor([t_ext, t_sm, t_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ext, t_sm, t_step = (float(x) for x in tt.tolist())
+    clocks = clk.summary()
+
+    peak, peak_src = measured_peaks()
+    b_ext, b_sm = algorithmic_bytes(V, b, P, Q, S)
+    value = V / (t_step * 1e-3)
+    ext_vps = V / (t_ext * 1e-3)
+    sm_ptit = P * T / (t_sm * 1e-3)
+    ext_gbs = b_ext / (t_ext * 1e-3) / 1e9
+    # dominant kernel: k_smooth (T launches per step) -- achieved = B_sm per launch / avg launch time
+    per_launch_ms = t_sm / max(T, 1)
+    sm_gbs = b_sm / (per_launch_ms * 1e-3) / 1e9
+    dominant = "k_smooth" if t_sm >= t_ext else "extraction (k_count+k_scan+k_emit)"
+    roof = {"bound": "hbm", "kernel": "k_smooth", "achieved": sm_gbs / world, "peak": peak, "unit": "GB/s",
+            "frac": sm_gbs / world / peak, "traffic": profile_traffic("k_smooth", cfg), "peak_source": peak_src,
+            "bytes_per_launch": b_sm / world, "launch_ms": per_launch_ms,
+            "note": "achieved = algorithmic bytes per launch (24P + 4(P+1) + 4S, per GPU) / average k_smooth launch time "
+                    "(CUDA events around the T back-to-back launches of each step, divided by T)"}
+    if dominant != "k_smooth":
+        roof["note"] += "; extraction dominated this config's step, see extract.frac"
+
+    # ---------------------------------------------------------------- e2e through the public host-buffer API
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host = torch.empty(labels.shape, dtype=labels.dtype, pin_memory=True)
+        host.copy_(labels)
+        state = {}
+        surface_nets_host(psn, host, sp, T, lam, d, state=state)
+        torch.cuda.synchronize()
+        ke = max(1, min(K, args.e2e_steps))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(ke):
+            surface_nets_host(psn, host, sp, T, lam, d, state=state)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / ke
+        e2e = {"value": V / (te * 1e-3), "unit": "voxel/s", "h2d_bytes_per_step": int(state["h2d_bytes"]),
+               "d2h_bytes_per_step": int(state["d2h_bytes"]), "ms_per_step": te, "steps": ke,
+               "api": "paper_2401_14906_b200.psn.surface_nets_host (pinned host labels -> device -> pinned host mesh)"}
+        del host, state
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            n_layers = max(1, int(round(args.cpu_voxels / (M * N))))
+            dt, vox, (k0, k1), _ = oracle_sample(cfg, n_layers,
+                                                 labels_host=lambda a, b_: labels[a:b_].cpu().numpy())
+            cpu = {"value": vox / dt, "unit": "voxel/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{cfg} voxel layers [{k0},{k1}) ({vox} voxels, {dt:.1f} s): oracle extract + {T}-iteration fp64 smoothing, single thread"}
+        except Exception as e:  # never fail the bench on the baseline leg
+            cpu = {"value": None, "unit": "voxel/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        l2 = 126e6
+        line = {
+            "metric": METRIC, "value": value, "unit": "voxel/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": {1: "u8", 2: "u16", 4: "u32"}[b] + "/f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[cfg], "dims": [M, N, O], "label_bytes": b, "iterations": T,
+                       "relaxation": lam, "constraint_voxels": d, "spacing": list(sp),
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "l2": ("inputs larger than L2 (%.2f GB labels, %.2f GB smoothing state)" % (V * b / 1e9, P * 28 / 1e9))
+                       if V * b > l2 else "inputs fit in L2 (no flush; absolute numbers only)"},
+            "counts": {"points": P, "quads": Q, "stencil": S},
+            "extract": {"ms": t_ext, "voxels_per_s": ext_vps, "bytes_alg": b_ext, "gbs": ext_gbs, "frac": ext_gbs / world / peak},
+            "smooth": {"ms": t_sm, "pt_iters_per_s": sm_ptit, "bytes_alg_per_iter": b_sm, "gbs": sm_gbs,
+                       "frac": sm_gbs / world / peak},
+            "roofline": roof,
+            "gpu_launches": launches * K if world == 1 else None,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="psn", choices=["psn", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-voxels", type=float, default=24e6, help="oracle sample size for cpu_baseline")
+    ap.add_argument("--ref-voxels", type=float, default=6e6, help="oracle sample size per reference step")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "reference":
+            if rank == 0:
+                run_reference(args, rank, world)
+            return
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        try:
+            run_psn(args, rank, world, local_rank)
+        finally:
+            dist.destroy_process_group()
+        return
+    if args.impl == "reference":
+        run_reference(args, 0, 1)
+    else:
+        run_psn(args, 0, 1, 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -2,54 +2,69 @@
 //
 // PAPER sec 2.3: Pass 1 classifies x-edges and trims rows, Pass 2
 // classifies y/z-edges and adjusts the trim, Pass 3 combines
-// them into the per-voxel edge case, point / quad / stencil counts per voxel
-// row.  Here all three are one z-marching kernel:
+// them into the per-voxel edge case and the point / quad / stencil counts of
+// each voxel row.  All three run in one z-marching kernel:
 //
-//   CTA  = a block of TJ voxel rows (j0..j0+TJ-1) x up to 1024 x-positions,
-//          marching over a z-chunk of voxel layers [kbeg, kend).
-//   lane = a chunk of 4 lattice points (x0..x0+3) of the TJ+1 grid rows of
-//          the current two lattice slices, kept in registers (packed words).
+//   CTA   = TJ voxel rows (j0..j0+TJ-1) x up to 1024 x-positions, marching
+//           over a z-chunk of voxel layers [kbeg, kend).
+//   stage = the TJ+1 grid rows of one lattice slice, staged in shared memory
+//           by the TMA engine (cp.async.bulk, one bulk copy per row) in a
+//           4-deep ring completed on mbarriers, so HBM streams while the SMs
+//           classify the previous slices.
+//   lane  = a chunk of 4 consecutive x positions (packed words).
 //
-// Fast path (the GPU analogue of the paper's computational trimming):
-// a lane's 4 voxels of a voxel row are uniform -- no edge, no point -- iff its
-// four grid-row chunks are internally constant (x-equal incl. the next element)
-// and equal to each other; a warp whose 32 lanes are all uniform skips the row
-// with ~5 instructions.  Otherwise the slow path builds the 12 edge planes
-// (X/Y/Z, SPREAD form), the six face planes (c^f) and the point plane
-// (c^e != 0), and counts with popc.
+// Per layer each thread first runs the FAST test on its chunk for every row:
+// the chunk's four grid rows are x-constant (incl. the next element) and equal
+// to each other -> no intersected edge, no point (the GPU analogue of the
+// paper's computational trimming: "rapidly skip portions of rows,
+// entire rows, and even entire data slices").  The surviving (row, chunk)
+// pairs are COMPACTED into a per-warp queue and processed with full lanes by
+// the SWAR slow path, which builds the 12 edge planes (X/Y/Z), the six face
+// planes (c^f), the point plane (c^e != 0) and counts with popc.
 //
 // Outputs per voxel row r = j + (N-1)(k - kA): cntP/cntQ/cntS (halo layers
-// count points only), the point trim [xL, xR) (P:124's final trim, in voxel
-// units; [0,0) when empty) and the point bit-planes pmask[r][chunk][4]
-// (de-interleaved: word p, bit l <-> voxel 128*chunk + 4*l + p).
+// count points only), the point trim [xL, xR) (P:124's final trim in voxel
+// units; [0,0) when empty) and the point bit-plane pmask[r][w] in natural
+// order (bit b of word w <-> voxel 32w + b).
 #pragma once
 #include "psn_common.cuh"
 
 namespace psn {
+
+constexpr int kCountStages = 4;
 
 struct CountArgs {
     const void *labels;
     int64_t M, N, O, z_lo;
     int64_t kA, kB;            // counted voxel layers (own plus halo)
     int64_t own_k0, own_k1;
-    int64_t W4;                // 128-voxel chunks per row
+    int64_t W32;               // 32-voxel words per row of pmask
     int64_t nXT, nJB, KZ;      // grid decomposition
+    int64_t RB;                // bytes per staged row buffer (multiple of 16)
     uint32_t *cntP, *cntQ, *cntS;
     int2 *trim;
     uint32_t *pmask;
     LabelSet ls;
     int multi_xt;              // several x-tiles per row: accumulate with global atomics
+    int tma;                   // rows are 16-byte aligned: stage with cp.async.bulk
 };
 
-template <typename T, int TJ, bool ANZ, bool VEC>
+template <typename T> constexpr int count_tj() { return sizeof(T) == 1 ? 16 : (sizeof(T) == 2 ? 8 : 4); }
+
+template <typename T, int TJ, bool ANZ>
 __global__ void __launch_bounds__(256) k_count(CountArgs a) {
-    constexpr int NW = Pack<T>::NW;
-    constexpr uint32_t MSB = Pack<T>::MSB;
+    constexpr int NW = Pack<T>::NW, NS = kCountStages, EB = Pack<T>::EB, EPW = Pack<T>::EPW;
+    constexpr int XT = 1024;                       // x positions per CTA
+    constexpr int XPAD = 16 / (int)sizeof(T);      // extra elements staged (next element + 16-B rounding)
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ __align__(8) uint64_t bars[NS];
     __shared__ uint32_t sP[2][TJ], sQ[2][TJ], sS[2][TJ];
     __shared__ int sL[2][TJ], sR[2][TJ];
+    __shared__ uint32_t spm[2][TJ][32];
+    __shared__ uint16_t squeue[8][32 * TJ];
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t bid = blockIdx.x;
     const int64_t xt = bid % a.nXT;
     const int64_t jb = (bid / a.nXT) % a.nJB;
@@ -58,150 +73,215 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
     const int64_t kbeg = a.kA + zc * a.KZ;
     const int64_t kend = min(kbeg + a.KZ, a.kB);
     const int64_t M = a.M, N = a.N;
-    const int64_t x0 = xt * 1024 + 4 * (int64_t)threadIdx.x;
-    const int64_t chunk = (xt * 1024 + 128 * (int64_t)warp) >> 7;
-    const bool chunk_live = chunk < a.W4;
+    const int64_t x_t0 = xt * XT;
+    const int64_t xlen = min((int64_t)(XT + XPAD), M - x_t0);   // staged elements per row
+    const uint32_t copy_bytes = (uint32_t)(xlen * (int64_t)sizeof(T));
+    const int64_t RB = a.RB;
+    const int64_t stage_bytes = (TJ + 1) * RB;
+    const int64_t x0 = x_t0 + 4 * (int64_t)tid;   // this thread's chunk
+    const bool chunk_has_voxel = x0 <= M - 2;
 
     LabelSet ls = a.ls;
     if (!ANZ && sizeof(T) < 4) {
-        for (int t = threadIdx.x; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
+        for (int t = tid; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
         ls.bits = sbits;
     }
-    if (threadIdx.x < 2 * TJ) {
-        int s = threadIdx.x / TJ, r = threadIdx.x % TJ;
+    for (int t = tid; t < 2 * TJ; t += blockDim.x) {
+        const int s = t / TJ, r = t % TJ;
         sP[s][r] = 0; sQ[s][r] = 0; sS[s][r] = 0; sL[s][r] = 0x7fffffff; sR[s][r] = -1;
+    }
+    for (int t = tid; t < 2 * TJ * 32; t += blockDim.x) (&spm[0][0][0])[t] = 0u;
+    for (int64_t t = tid; t < NS * stage_bytes / 16; t += blockDim.x)
+        reinterpret_cast<uint4 *>(dsm)[t] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
     }
     __syncthreads();
     if (kbeg >= kend) return;
-
-    // spread masks of this lane's 4 elements: voxel exists / has a -x / +x neighbour
-    uint32_t mvox[NW], mi1[NW], miM3[NW];
-#pragma unroll
-    for (int q = 0; q < NW; ++q) { mvox[q] = 0; mi1[q] = 0; miM3[q] = 0; }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const uint32_t bit = 1u << ((Pack<T>::EB * (e % Pack<T>::EPW) + Pack<T>::EB - 1) & 31);
-        const int64_t i = x0 + e;
-        if (i <= M - 2) mvox[e / Pack<T>::EPW] |= bit;
-        if (i >= 1) mi1[e / Pack<T>::EPW] |= bit;
-        if (i <= M - 3) miM3[e / Pack<T>::EPW] |= bit;
-    }
+    const int64_t nsteps = kend - kbeg;           // voxel layers; slices kbeg..kend
 
     const T *lab = reinterpret_cast<const T *>(a.labels);
-    uint32_t W0[TJ + 1][NW], H0[TJ + 1][NW], W1[TJ + 1][NW], H1[TJ + 1][NW];
-    bool X0[TJ + 1], X1[TJ + 1];
+    auto row_src = [&](int64_t s, int g) -> const T * {
+        const int64_t j = min(j0 + g, N - 1);
+        return lab + ((s - a.z_lo) * N + j) * M + x_t0;
+    };
+    // Fill the stage of slice ordinal o (slice kbeg + o).  TMA: one elected
+    // thread; fallback (rows not 16-B aligned): all threads copy.
+    auto fill = [&](int64_t o) {
+        const int st = (int)(o % NS);
+        uint8_t *base = dsm + st * stage_bytes;
+        if (a.tma) {
+            if (tid == 0) {
+                fence_proxy_async();   // prior generic reads of this stage precede the async-proxy writes
+                mbar_expect_tx(&bars[st], copy_bytes * (TJ + 1));
+#pragma unroll 1
+                for (int g = 0; g <= TJ; ++g)
+                    tma_load_1d(base + g * RB, row_src(kbeg + o, g), copy_bytes, &bars[st]);
+            }
+        } else {
+            for (int64_t t = tid; t < (TJ + 1) * xlen; t += blockDim.x) {
+                const int g = (int)(t / xlen);
+                const int64_t x = t % xlen;
+                reinterpret_cast<T *>(base + g * RB)[x] = row_src(kbeg + o, g)[x];
+            }
+        }
+    };
+    auto wait = [&](int64_t o) {
+        if (a.tma) mbar_wait(&bars[o % NS], (uint32_t)((o / NS) & 1));
+    };
+    for (int64_t o = 0; o < NS && o <= nsteps; ++o) fill(o);
+    if (!a.tma) __syncthreads();
 
-    // Load the TJ+1 grid-row chunks of lattice slice k (plus the element after
-    // each chunk), their one-element shift, and the x-uniform flag.
-    auto load_slice = [&](uint32_t (&Wd)[TJ + 1][NW], uint32_t (&Hd)[TJ + 1][NW], bool (&Xd)[TJ + 1],
-                          int64_t k) {
+    auto chunk_at = [&](int64_t o, int g, int64_t c, uint32_t (&w)[NW], uint32_t &nxt) {
+        const uint8_t *p = dsm + (o % NS) * stage_bytes + g * RB + 4 * c * (int64_t)sizeof(T);
+        if constexpr (NW == 1) { w[0] = *reinterpret_cast<const uint32_t *>(p); }
+        else if constexpr (NW == 2) { uint2 v = *reinterpret_cast<const uint2 *>(p); w[0] = v.x; w[1] = v.y; }
+        else { uint4 v = *reinterpret_cast<const uint4 *>(p); w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
+        nxt = *reinterpret_cast<const uint32_t *>(p + 4 * sizeof(T));
+        if (!ANZ) { remap<T>(ls, w); nxt = remap1<T>(ls, nxt); }
+    };
+
+    // Per-slice flags of this thread's chunk: huM bit g = row g x-constant
+    // (incl. the next element); eqYM bit g = rows g and g+1 equal.
+    uint32_t Wa[TJ + 1][NW], Wb[TJ + 1][NW];
+    uint32_t huA = 0, eqA = 0, huB = 0, eqB = 0;
+    auto load_flags = [&](int64_t o, uint32_t (&W)[TJ + 1][NW], uint32_t &hu, uint32_t &eqy) {
+        hu = 0; eqy = 0;
 #pragma unroll
-        for (int r = 0; r <= TJ; ++r) {
-            const int64_t j = min(j0 + r, N - 1);
-            const T *row = lab + ((k - a.z_lo) * N + j) * M;
-            uint32_t w[NW];
-            load_chunk<T, VEC>(row, x0, M, w);
-            if (!ANZ) remap<T>(ls, w);
-            uint32_t nxt = __shfl_down_sync(kFull, w[0], 1);
-            if (lane == 31) {
-                nxt = load_word<T, VEC>(row, x0 + 4, M);
-                if (!ANZ) nxt = remap1<T>(ls, nxt);
-            }
-            uint32_t h[NW];
-            shift1<T>(w, nxt, h);
-            bool ex = true;
+        for (int g = 0; g <= TJ; ++g) {
+            uint32_t nxt, h[NW];
+            chunk_at(o, g, tid, W[g], nxt);
+            shift1<T>(W[g], nxt, h);
+            bool e = true;
 #pragma unroll
-            for (int q = 0; q < NW; ++q) {
-                Wd[r][q] = w[q]; Hd[r][q] = h[q];
-                ex = ex && (w[q] == h[q]);
-            }
-            Xd[r] = ex;
+            for (int q = 0; q < NW; ++q) e = e && (W[g][q] == h[q]);
+            hu |= (e ? 1u : 0u) << g;
+        }
+#pragma unroll
+        for (int g = 0; g < TJ; ++g) {
+            bool e = true;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) e = e && (W[g][q] == W[g + 1][q]);
+            eqy |= (e ? 1u : 0u) << g;
         }
     };
 
-    // Voxel layer k from slices k (lo) and k+1 (hi).
-    auto process = [&](const uint32_t (&Wl)[TJ + 1][NW], const uint32_t (&Hl)[TJ + 1][NW], const bool (&Xl)[TJ + 1],
-                       const uint32_t (&Wh)[TJ + 1][NW], const uint32_t (&Hh)[TJ + 1][NW], const bool (&Xh)[TJ + 1],
-                       int64_t k, int slot) {
+    const int64_t nrows = N - 1 - j0;   // voxel rows of this block (may be < TJ at the edge)
+    const uint32_t rows_valid = (nrows >= TJ) ? ((1u << TJ) - 1u) : ((1u << (uint32_t)(nrows > 0 ? nrows : 0)) - 1u);
+
+    // Slow path for one (row r, chunk c) task of voxel layer k (slices o, o+1).
+    auto process_task = [&](int64_t o, int r, int c, int64_t k, bool own, int slot) {
+        uint32_t A[NW], B[NW], C[NW], D[NW], hA[NW], hB[NW], hC[NW], hD[NW], n;
+        chunk_at(o, r, c, A, n); shift1<T>(A, n, hA);
+        chunk_at(o, r + 1, c, B, n); shift1<T>(B, n, hB);
+        chunk_at(o + 1, r, c, C, n); shift1<T>(C, n, hC);
+        chunk_at(o + 1, r + 1, c, D, n); shift1<T>(D, n, hD);
+        const int64_t xc = x_t0 + 4 * (int64_t)c, j = j0 + r;
+        uint32_t mvox[NW], mi1[NW], miM3[NW];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) { mvox[q] = 0; mi1[q] = 0; miM3[q] = 0; }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t bit = 1u << ((EB * (e % EPW) + EB - 1) & 31);
+            const int64_t i = xc + e;
+            if (i <= M - 2) mvox[e / EPW] |= bit;
+            if (i >= 1) mi1[e / EPW] |= bit;
+            if (i <= M - 3) miM3[e / EPW] |= bit;
+        }
+        uint32_t pt[NW], cq = 0, cs = 0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            const uint32_t XA = neq<T>(A[q], hA[q]), XB = neq<T>(B[q], hB[q]);
+            const uint32_t XC = neq<T>(C[q], hC[q]), XD = neq<T>(D[q], hD[q]);
+            const uint32_t YAB = neq<T>(A[q], B[q]), YCD = neq<T>(C[q], D[q]);
+            const uint32_t ZAC = neq<T>(A[q], C[q]), ZBD = neq<T>(B[q], D[q]);
+            const uint32_t YABs = neq<T>(hA[q], hB[q]), YCDs = neq<T>(hC[q], hD[q]);
+            const uint32_t ZACs = neq<T>(hA[q], hC[q]), ZBDs = neq<T>(hB[q], hD[q]);
+            const uint32_t Fmx = YAB | YCD | ZAC | ZBD;
+            const uint32_t Fpx = YABs | YCDs | ZACs | ZBDs;
+            const uint32_t Fmy = XA | XC | ZAC | ZACs;
+            const uint32_t Fpy = XB | XD | ZBD | ZBDs;
+            const uint32_t Fmz = XA | XB | YAB | YABs;
+            const uint32_t Fpz = XC | XD | YCD | YCDs;
+            pt[q] = (Fmx | Fpx | Fmy | Fpy | Fmz | Fpz) & mvox[q];
+            if (own) {
+                if (j >= 1 && k >= 1) cq += __popc(XA & mvox[q]);
+                if (k >= 1) cq += __popc(YAB & mvox[q] & mi1[q]);
+                if (j >= 1) cq += __popc(ZAC & mvox[q] & mi1[q]);
+                if (k >= 1) cs += __popc(Fmz & mvox[q]);
+                if (j >= 1) cs += __popc(Fmy & mvox[q]);
+                cs += __popc(Fmx & mvox[q] & mi1[q]);
+                cs += __popc(Fpx & miM3[q]);
+                if (j <= N - 3) cs += __popc(Fpy & mvox[q]);
+                if (k <= a.O - 3) cs += __popc(Fpz & mvox[q]);
+            }
+        }
+        uint32_t nib = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) nib |= flag<T>(pt, e) << e;
+        if (nib) {
+            atomicAdd(&sP[slot][r], (uint32_t)__popc(nib));
+            atomicAdd(&sQ[slot][r], cq);
+            atomicAdd(&sS[slot][r], cs);
+            atomicOr(&spm[slot][r][c >> 3], nib << (4 * (c & 7)));
+            atomicMin(&sL[slot][r], (int)(xc + __ffs(nib) - 1));
+            atomicMax(&sR[slot][r], (int)(xc + 31 - __clz(nib)));
+        }
+    };
+
+    auto step = [&](int64_t o, const uint32_t (&Wl)[TJ + 1][NW], uint32_t hul, uint32_t eql,
+                    const uint32_t (&Wh)[TJ + 1][NW], uint32_t huh, uint32_t eqh) {
+        const int64_t k = kbeg + o;
+        const int slot = (int)(o & 1);
         const bool own = (k >= a.own_k0) && (k < a.own_k1);
+        uint32_t eqz = 0;
 #pragma unroll
         for (int r = 0; r < TJ; ++r) {
-            const int64_t j = j0 + r;
-            if (j > N - 2) break;
-            bool uni = Xl[r] && Xl[r + 1] && Xh[r] && Xh[r + 1];
+            bool e = true;
 #pragma unroll
-            for (int q = 0; q < NW; ++q)
-                uni = uni && (Wl[r][q] == Wl[r + 1][q]) && (Wh[r][q] == Wh[r + 1][q]) && (Wl[r][q] == Wh[r][q]);
-            const int64_t rr = j + (N - 1) * (k - a.kA);
-            uint32_t *pm = a.pmask + (rr * a.W4 + chunk) * 4;
-            if (__all_sync(kFull, uni)) {
-                if (chunk_live && lane < 4) pm[lane] = 0u;
-                continue;
+            for (int q = 0; q < NW; ++q) e = e && (Wl[r][q] == Wh[r][q]);
+            eqz |= (e ? 1u : 0u) << r;
+        }
+        const uint32_t uni = hul & (hul >> 1) & huh & (huh >> 1) & eql & eqh & eqz;
+        const uint32_t slow = chunk_has_voxel ? (~uni & rows_valid) : 0u;
+        // compact the slow (row, chunk) tasks of this warp
+        const uint32_t cnt = __popc(slow);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        if (total) {
+            uint32_t pos = incl - cnt, m = slow;
+            while (m) {
+                const int r = __ffs(m) - 1;
+                m &= m - 1;
+                squeue[warp][pos++] = (uint16_t)(r * 32 + lane);
             }
-            uint32_t pt[NW];
-            uint32_t cq = 0, cs = 0, cp = 0;
-#pragma unroll
-            for (int q = 0; q < NW; ++q) {
-                const uint32_t A = Wl[r][q], B = Wl[r + 1][q], C = Wh[r][q], D = Wh[r + 1][q];
-                const uint32_t hA = Hl[r][q], hB = Hl[r + 1][q], hC = Hh[r][q], hD = Hh[r + 1][q];
-                const uint32_t XA = neq<T>(A, hA), XB = neq<T>(B, hB);
-                const uint32_t XC = neq<T>(C, hC), XD = neq<T>(D, hD);
-                const uint32_t YAB = neq<T>(A, B), YCD = neq<T>(C, D);
-                const uint32_t ZAC = neq<T>(A, C), ZBD = neq<T>(B, D);
-                const uint32_t YABs = neq<T>(hA, hB), YCDs = neq<T>(hC, hD);
-                const uint32_t ZACs = neq<T>(hA, hC), ZBDs = neq<T>(hB, hD);
-                const uint32_t Fmx = YAB | YCD | ZAC | ZBD;
-                const uint32_t Fpx = YABs | YCDs | ZACs | ZBDs;
-                const uint32_t Fmy = XA | XC | ZAC | ZACs;
-                const uint32_t Fpy = XB | XD | ZBD | ZBDs;
-                const uint32_t Fmz = XA | XB | YAB | YABs;
-                const uint32_t Fpz = XC | XD | YCD | YCDs;
-                pt[q] = (Fmx | Fpx | Fmy | Fpy | Fmz | Fpz) & mvox[q];
-                cp += __popc(pt[q]);
-                if (own) {
-                    if (j >= 1 && k >= 1) cq += __popc(XA & mvox[q]);
-                    if (k >= 1) cq += __popc(YAB & mvox[q] & mi1[q]);
-                    if (j >= 1) cq += __popc(ZAC & mvox[q] & mi1[q]);
-                    if (k >= 1) cs += __popc(Fmz & mvox[q]);
-                    if (j >= 1) cs += __popc(Fmy & mvox[q]);
-                    cs += __popc(Fmx & mvox[q] & mi1[q]);
-                    cs += __popc(Fpx & miM3[q]);
-                    if (j <= N - 3) cs += __popc(Fpy & mvox[q]);
-                    if (k <= a.O - 3) cs += __popc(Fpz & mvox[q]);
-                }
-            }
-            // point bit-planes (de-interleaved by element position)
-            const uint32_t b0 = __ballot_sync(kFull, flag<T>(pt, 0));
-            const uint32_t b1 = __ballot_sync(kFull, flag<T>(pt, 1));
-            const uint32_t b2 = __ballot_sync(kFull, flag<T>(pt, 2));
-            const uint32_t b3 = __ballot_sync(kFull, flag<T>(pt, 3));
-            if (chunk_live && lane < 4) pm[lane] = lane == 0 ? b0 : lane == 1 ? b1 : lane == 2 ? b2 : b3;
-            // trim: first / last point voxel of this lane
-            int first = 0x7fffffff, last = -1;
-#pragma unroll
-            for (int e = 3; e >= 0; --e) if (flag<T>(pt, e)) first = (int)(x0 + e);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) if (flag<T>(pt, e)) last = (int)(x0 + e);
-            cp = __reduce_add_sync(kFull, cp);
-            cq = __reduce_add_sync(kFull, cq);
-            cs = __reduce_add_sync(kFull, cs);
-            first = __reduce_min_sync(kFull, first);
-            last = __reduce_max_sync(kFull, last);
-            if (lane == 0 && cp) {
-                atomicAdd(&sP[slot][r], cp);
-                atomicAdd(&sQ[slot][r], cq);
-                atomicAdd(&sS[slot][r], cs);
-                atomicMin(&sL[slot][r], first);
-                atomicMax(&sR[slot][r], last);
+            __syncwarp();
+            for (uint32_t t = lane; t < total; t += 32) {
+                const uint32_t task = squeue[warp][t];
+                process_task(o, (int)(task >> 5), warp * 32 + (int)(task & 31), k, own, slot);
             }
         }
         __syncthreads();
-        // flush this layer's TJ row counters (double-buffered slots: one barrier per layer)
-        if (threadIdx.x < TJ) {
-            const int r = threadIdx.x;
-            const int64_t j = j0 + r;
-            if (j <= N - 2) {
-                const int64_t rr = j + (N - 1) * (k - a.kA);
+        // flush this layer's rows (double-buffered slots: one barrier per layer)
+        for (int t = tid; t < TJ * 32; t += blockDim.x) {
+            const int r = t >> 5, w = t & 31;
+            const int64_t gw = (x_t0 >> 5) + w;
+            if (((rows_valid >> r) & 1u) && gw < a.W32) {
+                const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
+                a.pmask[rr * a.W32 + gw] = spm[slot][r][w];
+            }
+            spm[slot][r][w] = 0u;
+        }
+        if (tid < TJ) {
+            const int r = tid;
+            if ((rows_valid >> r) & 1u) {
+                const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
                 const uint32_t p = sP[slot][r];
                 const int xl = p ? sL[slot][r] : 0, xr = p ? sR[slot][r] + 1 : 0;
                 if (!a.multi_xt) {
@@ -215,15 +295,20 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
             }
             sP[slot][r] = 0; sQ[slot][r] = 0; sS[slot][r] = 0; sL[slot][r] = 0x7fffffff; sR[slot][r] = -1;
         }
+        // slice o is no longer read: refill its stage with slice o + NS
+        if (o + NS <= nsteps) fill(o + NS);
     };
 
-    load_slice(W0, H0, X0, kbeg);
-    for (int64_t k = kbeg; k < kend; k += 2) {
-        load_slice(W1, H1, X1, k + 1);
-        process(W0, H0, X0, W1, H1, X1, k, 0);
-        if (k + 1 >= kend) break;
-        load_slice(W0, H0, X0, k + 2);
-        process(W1, H1, X1, W0, H0, X0, k + 1, 1);
+    wait(0);
+    load_flags(0, Wa, huA, eqA);
+    for (int64_t o = 0; o < nsteps; o += 2) {
+        wait(o + 1);
+        load_flags(o + 1, Wb, huB, eqB);
+        step(o, Wa, huA, eqA, Wb, huB, eqB);
+        if (o + 1 >= nsteps) break;
+        wait(o + 2);
+        load_flags(o + 2, Wa, huA, eqA);
+        step(o + 1, Wb, huB, eqB, Wa, huA, eqA);
     }
 }
 

@@ -1,17 +1,18 @@
 // k_emit.cuh -- Pass 4 of PSN extraction on sm_100a.
 //
-// One warp per voxel row V_{j,k} (grid-stride), walking the row's 128-voxel
-// chunks left to right.  The paper's 3x3 voxel-row iterator (Fig. 6)
-// becomes a prefix-popc over the stored point bit-planes of the needed
-// neighbour rows: every voxel's point id, and the ids of the neighbours its
-// quads and stencil reference, are
-//     window_base + offP[row'] + (points of row' before this chunk)
-//                 + popc(planes of row' below this voxel inside the chunk).
-// Quads use rows (j-1,k-1), (j,k-1), (j-1,k); the stencil adds (j+1,k) and
-// (j,k+1).  Chunks with no point are skipped without touching the labels
-// ("the trim interval plays an important role ... to rapidly skip data").
-// All writes land in disjoint, preallocated slots given by the scan -- no
-// atomics, no locks.
+// One warp per voxel row V_{j,k} (grid-stride).  The paper's 3x3 voxel-row
+// iterator (Fig. 6) becomes prefix-popcounts over the natural-order
+// point bit-planes written by k_count: the id of voxel i of row r' is
+//     window_base + offP[r'] + popc(points of r' before i)
+// computed per 32-voxel word with a warp scan.  Quads use rows (j-1,k-1),
+// (j,k-1), (j-1,k); the stencil adds (j+1,k) and (j,k+1).
+//
+// Work is at POINT granularity: the row's points are compacted into a
+// per-warp list and processed 32 at a time, one point per lane, so voxels
+// without a point cost nothing ("rapidly skip data").  Each point reads
+// its 8 corner labels, forms the 12 edge predicates, the face mask (c^f,
+// P:118), its owned quads (open boundaries P:264) and writes them into
+// the disjoint preallocated slots given by the scan -- no atomics.
 #pragma once
 #include "k_scan.cuh"
 #include "psn_common.cuh"
@@ -21,7 +22,7 @@ namespace psn {
 struct EmitArgs {
     const void *labels;
     int64_t M, N, O, z_lo;
-    int64_t kA, kB, own_k0, own_k1, W4, R;
+    int64_t kA, kB, own_k0, own_k1, W32, R;
     const uint32_t *cntP, *offP, *offQ, *offS, *pmask;
     LabelSet ls;
     double sp[3], org[3];
@@ -38,26 +39,22 @@ __device__ __forceinline__ float anchor_coord(double org, double sp, int64_t idx
     return __double2float_rn(__dadd_rn(org, __dmul_rn(__dadd_rn((double)idx, 0.5), sp)));
 }
 
-__device__ __forceinline__ uint32_t popc4(uint4 m, uint32_t lt) {
-    return __popc(m.x & lt) + __popc(m.y & lt) + __popc(m.z & lt) + __popc(m.w & lt);
-}
-__device__ __forceinline__ uint32_t bitp(uint4 m, int p, int lane) {
-    uint32_t w = p == 0 ? m.x : p == 1 ? m.y : p == 2 ? m.z : m.w;
-    return (w >> lane) & 1u;
-}
-__device__ __forceinline__ uint32_t popc_all(uint4 m) {
-    return __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
-}
-__device__ __forceinline__ uint4 ld_mask(const uint32_t *pm, int64_t row, int64_t W4, int64_t c) {
-    if (row < 0) return make_uint4(0, 0, 0, 0);
-    return __ldg(reinterpret_cast<const uint4 *>(pm + (row * W4 + c) * 4));
+template <typename T, bool ANZ>
+__device__ __forceinline__ uint32_t code_at(const T *p, const LabelSet &ls) {
+    uint32_t v = (uint32_t)__ldg(p);
+    if (!ANZ && !ls.identity) v = in_L<T>(ls, v) ? v : ls.z;
+    return v;
 }
 
-template <typename T, bool ANZ, bool VEC>
+constexpr int kEmitWarps = 8;
+
+template <typename T, bool ANZ>
 __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
-    constexpr int NW = Pack<T>::NW;
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
-    const int lane = threadIdx.x & 31;
+    __shared__ uint16_t slist[kEmitWarps][1024];      // point x positions of the current 1024-voxel block
+    __shared__ uint32_t sword[kEmitWarps][5][32];     // neighbour rows: mask word
+    __shared__ uint32_t spre[kEmitWarps][5][32];      // neighbour rows: points before the word
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     LabelSet ls = a.ls;
     if (!ANZ && sizeof(T) < 4) {
         for (int t = threadIdx.x; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
@@ -77,177 +74,160 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
         a.csr_off[before_hi - halo_lo] = a.first_stencil + (uint32_t)totS;   // CSR sentinel entry
     }
     const uint32_t gid_base = a.first_point - (uint32_t)halo_lo;   // global id of window index 0
-    const int64_t M = a.M, N = a.N, NV = N - 1;
+    const int64_t M = a.M, N = a.N, NV = N - 1, W32 = a.W32;
     const T *lab = reinterpret_cast<const T *>(a.labels);
+    const uint32_t lt = (1u << lane) - 1u;
 
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t rr = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); rr < a.R; rr += warps) {
+    for (int64_t rr = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; rr < a.R; rr += warps) {
         if (__ldg(a.cntP + rr) == 0) continue;
         const int64_t j = rr % NV, k = a.kA + rr / NV;
         const bool own = (k >= a.own_k0) && (k < a.own_k1);
-        const int64_t n1 = (own && j >= 1 && k - 1 >= a.kA) ? rr - NV - 1 : -1;   // (j-1,k-1)
-        const int64_t n2 = (own && k - 1 >= a.kA) ? rr - NV : -1;                  // (j,  k-1)
-        const int64_t n3 = (own && j >= 1) ? rr - 1 : -1;                           // (j-1,k)
-        const int64_t n4 = (own && j + 1 <= N - 2) ? rr + 1 : -1;                   // (j+1,k)
-        const int64_t n5 = (own && k + 1 < a.kB) ? rr + NV : -1;                    // (j,  k+1)
+        int64_t nb[5];
+        nb[0] = (own && j >= 1 && k - 1 >= a.kA) ? rr - NV - 1 : -1;   // (j-1,k-1)
+        nb[1] = (own && k - 1 >= a.kA) ? rr - NV : -1;                  // (j,  k-1)
+        nb[2] = (own && j >= 1) ? rr - 1 : -1;                           // (j-1,k)
+        nb[3] = (own && j + 1 <= N - 2) ? rr + 1 : -1;                   // (j+1,k)
+        nb[4] = (own && k + 1 < a.kB) ? rr + NV : -1;                    // (j,  k+1)
         const uint32_t offP = __ldg(a.offP + rr);
-        const uint32_t b1 = n1 >= 0 ? __ldg(a.offP + n1) : 0u, b2 = n2 >= 0 ? __ldg(a.offP + n2) : 0u;
-        const uint32_t b3 = n3 >= 0 ? __ldg(a.offP + n3) : 0u, b4 = n4 >= 0 ? __ldg(a.offP + n4) : 0u;
-        const uint32_t b5 = n5 >= 0 ? __ldg(a.offP + n5) : 0u;
+        uint32_t nbase[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) nbase[q] = nb[q] >= 0 ? __ldg(a.offP + nb[q]) : 0u;
         const uint32_t qbase = own ? __ldg(a.offQ + rr) : 0u, sbase = own ? __ldg(a.offS + rr) : 0u;
-        uint32_t run_o = 0, run1 = 0, run2 = 0, run3 = 0, run4 = 0, run5 = 0, run_q = 0, run_s = 0;
+        uint32_t run_o = 0, run_q = 0, run_s = 0;
+        uint32_t run_n[5] = {0, 0, 0, 0, 0};
         const T *rowA = lab + ((k - a.z_lo) * N + j) * M;
         const T *rowB = rowA + M;
         const T *rowC = rowA + N * M;
         const T *rowD = rowC + M;
-        const uint32_t lt = (1u << lane) - 1u;
 
-        for (int64_t c = 0; c < a.W4; ++c) {
-            const uint4 po = ld_mask(a.pmask, rr, a.W4, c);
-            const uint4 m1 = ld_mask(a.pmask, n1, a.W4, c), m2 = ld_mask(a.pmask, n2, a.W4, c);
-            const uint4 m3 = ld_mask(a.pmask, n3, a.W4, c), m4 = ld_mask(a.pmask, n4, a.W4, c);
-            const uint4 m5 = ld_mask(a.pmask, n5, a.W4, c);
-            if (po.x | po.y | po.z | po.w) {
-                const int64_t x0 = 128 * c + 4 * lane;
-                uint32_t bits[4];
-                uint32_t np = 0;
+        for (int64_t w0 = 0; w0 < W32; w0 += 32) {
+            const int64_t w = w0 + lane;
+            const bool wok = w < W32;
+            const uint32_t om = wok ? __ldg(a.pmask + rr * W32 + w) : 0u;
+            // own points: exclusive scan of the word popcounts -> compact list
+            const uint32_t oc = __popc(om);
+            uint32_t oi = oc;
 #pragma unroll
-                for (int p = 0; p < 4; ++p) { bits[p] = bitp(po, p, lane); np += bits[p]; }
-                const uint32_t pre_o = run_o + popc4(po, lt);
-                if (!own) {
-                    // halo layer: points only (window entries needed by smoothing / triangulation)
-                    uint32_t acc = 0;
+            for (int d = 1; d < 32; d <<= 1) { const uint32_t y = __shfl_up_sync(kFull, oi, d); if (lane >= d) oi += y; }
+            const uint32_t blk_pts = __shfl_sync(kFull, oi, 31);
+            if (blk_pts == 0) {
+                if (own) {
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        if (!bits[p]) continue;
-                        const uint32_t w = offP + pre_o + acc++;
-                        a.points[3 * (int64_t)w + 0] = anchor_coord(a.org[0], a.sp[0], x0 + p);
-                        a.points[3 * (int64_t)w + 1] = anchor_coord(a.org[1], a.sp[1], j);
-                        a.points[3 * (int64_t)w + 2] = anchor_coord(a.org[2], a.sp[2], k);
+                    for (int q = 0; q < 5; ++q) {
+                        const uint32_t m = (nb[q] >= 0 && wok) ? __ldg(a.pmask + nb[q] * W32 + w) : 0u;
+                        run_n[q] += __reduce_add_sync(kFull, __popc(m));
                     }
-                } else {
-                    // labels of the voxel row's four grid rows (chunk + next element)
-                    uint32_t A[NW], B[NW], C[NW], D[NW], hA[NW], hB[NW], hC[NW], hD[NW];
-                    load_chunk<T, VEC>(rowA, x0, M, A);
-                    load_chunk<T, VEC>(rowB, x0, M, B);
-                    load_chunk<T, VEC>(rowC, x0, M, C);
-                    load_chunk<T, VEC>(rowD, x0, M, D);
-                    if (!ANZ) { remap<T>(ls, A); remap<T>(ls, B); remap<T>(ls, C); remap<T>(ls, D); }
-                    uint32_t nA = __shfl_down_sync(kFull, A[0], 1), nB = __shfl_down_sync(kFull, B[0], 1);
-                    uint32_t nC = __shfl_down_sync(kFull, C[0], 1), nD = __shfl_down_sync(kFull, D[0], 1);
-                    if (lane == 31) {
-                        nA = load_word<T, VEC>(rowA, x0 + 4, M); nB = load_word<T, VEC>(rowB, x0 + 4, M);
-                        nC = load_word<T, VEC>(rowC, x0 + 4, M); nD = load_word<T, VEC>(rowD, x0 + 4, M);
-                        if (!ANZ) { nA = remap1<T>(ls, nA); nB = remap1<T>(ls, nB); nC = remap1<T>(ls, nC); nD = remap1<T>(ls, nD); }
-                    }
-                    shift1<T>(A, nA, hA); shift1<T>(B, nB, hB); shift1<T>(C, nC, hC); shift1<T>(D, nD, hD);
-                    uint32_t XA[NW], YAB[NW], ZAC[NW], Fmx[NW], Fpx[NW], Fmy[NW], Fpy[NW], Fmz[NW], Fpz[NW];
-#pragma unroll
-                    for (int q = 0; q < NW; ++q) {
-                        XA[q] = neq<T>(A[q], hA[q]);
-                        const uint32_t XB = neq<T>(B[q], hB[q]), XC = neq<T>(C[q], hC[q]), XD = neq<T>(D[q], hD[q]);
-                        YAB[q] = neq<T>(A[q], B[q]);
-                        const uint32_t YCD = neq<T>(C[q], D[q]);
-                        ZAC[q] = neq<T>(A[q], C[q]);
-                        const uint32_t ZBD = neq<T>(B[q], D[q]);
-                        const uint32_t YABs = neq<T>(hA[q], hB[q]), YCDs = neq<T>(hC[q], hD[q]);
-                        const uint32_t ZACs = neq<T>(hA[q], hC[q]), ZBDs = neq<T>(hB[q], hD[q]);
-                        Fmx[q] = YAB[q] | YCD | ZAC[q] | ZBD;
-                        Fpx[q] = YABs | YCDs | ZACs | ZBDs;
-                        Fmy[q] = XA[q] | XC | ZAC[q] | ZACs;
-                        Fpy[q] = XB | XD | ZBD | ZBDs;
-                        Fmz[q] = XA[q] | XB | YAB[q] | YABs;
-                        Fpz[q] = XC | XD | YCD | YCDs;
-                    }
-                    uint32_t fm[4], qb[4];
-                    uint32_t nq = 0, ns = 0;
-#pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        const int64_t i = x0 + p;
-                        uint32_t f = 0, qq = 0;
-                        if (bits[p]) {
-                            f |= (flag<T>(Fmz, p) && k >= 1) ? 1u : 0u;
-                            f |= (flag<T>(Fmy, p) && j >= 1) ? 2u : 0u;
-                            f |= (flag<T>(Fmx, p) && i >= 1) ? 4u : 0u;
-                            f |= (flag<T>(Fpx, p) && i <= M - 3) ? 8u : 0u;
-                            f |= (flag<T>(Fpy, p) && j <= N - 3) ? 16u : 0u;
-                            f |= (flag<T>(Fpz, p) && k <= a.O - 3) ? 32u : 0u;
-                            qq |= (flag<T>(XA, p) && j >= 1 && k >= 1) ? 1u : 0u;
-                            qq |= (flag<T>(YAB, p) && i >= 1 && k >= 1) ? 2u : 0u;
-                            qq |= (flag<T>(ZAC, p) && i >= 1 && j >= 1) ? 4u : 0u;
-                        }
-                        fm[p] = f; qb[p] = qq;
-                        nq += __popc(qq); ns += __popc(f);
-                    }
-                    // warp exclusive scan of packed (points, quads, stencil entries)
-                    const uint32_t packed = (np << 20) | (nq << 10) | ns;
-                    uint32_t x = packed;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const uint32_t y = __shfl_up_sync(kFull, x, d);
-                        if (lane >= d) x += y;
-                    }
-                    const uint32_t tot = __shfl_sync(kFull, x, 31);
-                    const uint32_t ex = x - packed;
-                    uint32_t qslot = qbase + run_q + ((ex >> 10) & 1023u);
-                    uint32_t sslot = sbase + run_s + (ex & 1023u);
-                    const uint32_t p1 = b1 + run1 + popc4(m1, lt), p2 = b2 + run2 + popc4(m2, lt);
-                    const uint32_t p3 = b3 + run3 + popc4(m3, lt), p4 = b4 + run4 + popc4(m4, lt);
-                    const uint32_t p5 = b5 + run5 + popc4(m5, lt);
-                    uint32_t acc = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-#pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        if (bits[p]) {
-                            const int64_t i = x0 + p;
-                            const uint32_t w = offP + pre_o + acc;
-                            const uint32_t g = gid_base + w;
-                            const uint32_t g1 = gid_base + p1 + a1, g2 = gid_base + p2 + a2;
-                            const uint32_t g3 = gid_base + p3 + a3, g4 = gid_base + p4 + a4;
-                            const uint32_t g5 = gid_base + p5 + a5;
-                            a.points[3 * (int64_t)w + 0] = anchor_coord(a.org[0], a.sp[0], i);
-                            a.points[3 * (int64_t)w + 1] = anchor_coord(a.org[1], a.sp[1], j);
-                            a.points[3 * (int64_t)w + 2] = anchor_coord(a.org[2], a.sp[2], k);
-                            const uint32_t o = w - (uint32_t)halo_lo;
-                            a.fmask[o] = (uint8_t)fm[p];
-                            a.csr_off[o] = a.first_stencil + sslot;
-                            const uint32_t f = fm[p];
-                            if (f & 1u) a.csr_ids[sslot++] = g2;       // -z
-                            if (f & 2u) a.csr_ids[sslot++] = g3;       // -y
-                            if (f & 4u) a.csr_ids[sslot++] = g - 1u;   // -x
-                            if (f & 8u) a.csr_ids[sslot++] = g + 1u;   // +x
-                            if (f & 16u) a.csr_ids[sslot++] = g4;      // +y
-                            if (f & 32u) a.csr_ids[sslot++] = g5;      // +z
-                            const uint32_t cA = cls_of_code<T, ANZ>(ls, elem<T>(A, p));
-                            if (qb[p] & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
-                                *reinterpret_cast<uint4 *>(a.quads + 4 * (int64_t)qslot) = make_uint4(g1, g2, g, g3);
-                                *reinterpret_cast<uint2 *>(a.pairs + 2 * (int64_t)qslot) =
-                                    make_uint2(cA, cls_of_code<T, ANZ>(ls, elem<T>(hA, p)));
-                                ++qslot;
-                            }
-                            if (qb[p] & 2u) {   // y-quad [(i-1,k-1), (i-1,k), (i,k), (i,k-1)] in row j
-                                *reinterpret_cast<uint4 *>(a.quads + 4 * (int64_t)qslot) = make_uint4(g2 - 1u, g - 1u, g, g2);
-                                *reinterpret_cast<uint2 *>(a.pairs + 2 * (int64_t)qslot) =
-                                    make_uint2(cA, cls_of_code<T, ANZ>(ls, elem<T>(B, p)));
-                                ++qslot;
-                            }
-                            if (qb[p] & 4u) {   // z-quad [(i-1,j-1), (i,j-1), (i,j), (i-1,j)] in layer k
-                                *reinterpret_cast<uint4 *>(a.quads + 4 * (int64_t)qslot) = make_uint4(g3 - 1u, g3, g, g - 1u);
-                                *reinterpret_cast<uint2 *>(a.pairs + 2 * (int64_t)qslot) =
-                                    make_uint2(cA, cls_of_code<T, ANZ>(ls, elem<T>(C, p)));
-                                ++qslot;
-                            }
-                            ++acc;
-                        }
-                        a1 += bitp(m1, p, lane); a2 += bitp(m2, p, lane); a3 += bitp(m3, p, lane);
-                        a4 += bitp(m4, p, lane); a5 += bitp(m5, p, lane);
-                    }
-                    run_q += (tot >> 10) & 1023u;
-                    run_s += tot & 1023u;
+                }
+                continue;
+            }
+            {
+                uint32_t pos = oi - oc, m = om;
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    slist[warp][pos++] = (uint16_t)(lane * 32 + b);
                 }
             }
-            run_o += popc_all(po);
-            run1 += popc_all(m1); run2 += popc_all(m2); run3 += popc_all(m3);
-            run4 += popc_all(m4); run5 += popc_all(m5);
+            uint32_t blk_n[5] = {0, 0, 0, 0, 0};
+            if (own) {
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const uint32_t m = (nb[q] >= 0 && wok) ? __ldg(a.pmask + nb[q] * W32 + w) : 0u;
+                    const uint32_t c = __popc(m);
+                    uint32_t x = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) { const uint32_t y = __shfl_up_sync(kFull, x, d); if (lane >= d) x += y; }
+                    sword[warp][q][lane] = m;
+                    spre[warp][q][lane] = run_n[q] + x - c;
+                    blk_n[q] = __shfl_sync(kFull, x, 31);
+                }
+            }
+            __syncwarp();
+            for (uint32_t base = 0; base < blk_pts; base += 32) {
+                const uint32_t t = base + lane;
+                const bool act = t < blk_pts;
+                const uint32_t xb = act ? slist[warp][t] : 0u;          // position within the block
+                const int64_t i = w0 * 32 + xb;                          // voxel x
+                const uint32_t n = run_o + t;                            // index of the point in the row
+                const uint32_t wi = offP + n;                            // window index
+                const uint32_t g = gid_base + wi;                        // global id
+                uint32_t fm = 0, qb = 0, deg = 0;
+                uint32_t cA = 0, cA1 = 0, cB = 0, cC = 0;
+                uint32_t gn[5] = {0, 0, 0, 0, 0};
+                if (act && own) {
+                    const uint32_t A = code_at<T, ANZ>(rowA + i, ls), A1 = code_at<T, ANZ>(rowA + i + 1, ls);
+                    const uint32_t B = code_at<T, ANZ>(rowB + i, ls), B1 = code_at<T, ANZ>(rowB + i + 1, ls);
+                    const uint32_t C = code_at<T, ANZ>(rowC + i, ls), C1 = code_at<T, ANZ>(rowC + i + 1, ls);
+                    const uint32_t D = code_at<T, ANZ>(rowD + i, ls), D1 = code_at<T, ANZ>(rowD + i + 1, ls);
+                    const bool XA = A != A1, XB = B != B1, XC = C != C1, XD = D != D1;
+                    const bool YAB = A != B, YA1 = A1 != B1, YCD = C != D, YC1 = C1 != D1;
+                    const bool ZAC = A != C, ZA1 = A1 != C1, ZBD = B != D, ZB1 = B1 != D1;
+                    fm |= ((XA | XB | YAB | YA1) && k >= 1) ? 1u : 0u;          // -z
+                    fm |= ((XA | XC | ZAC | ZA1) && j >= 1) ? 2u : 0u;          // -y
+                    fm |= ((YAB | YCD | ZAC | ZBD) && i >= 1) ? 4u : 0u;        // -x
+                    fm |= ((YA1 | YC1 | ZA1 | ZB1) && i <= M - 3) ? 8u : 0u;    // +x
+                    fm |= ((XB | XD | ZBD | ZB1) && j <= N - 3) ? 16u : 0u;     // +y
+                    fm |= ((XC | XD | YCD | YC1) && k <= a.O - 3) ? 32u : 0u;   // +z
+                    qb |= (XA && j >= 1 && k >= 1) ? 1u : 0u;
+                    qb |= (YAB && i >= 1 && k >= 1) ? 2u : 0u;
+                    qb |= (ZAC && i >= 1 && j >= 1) ? 4u : 0u;
+                    deg = __popc(fm);
+                    cA = cls_of_code<T, ANZ>(ls, A); cA1 = cls_of_code<T, ANZ>(ls, A1);
+                    cB = cls_of_code<T, ANZ>(ls, B); cC = cls_of_code<T, ANZ>(ls, C);
+                    const int wl = (int)(xb >> 5);
+                    const uint32_t below = (1u << (xb & 31)) - 1u;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q)
+                        gn[q] = gid_base + nbase[q] + spre[warp][q][wl] + __popc(sword[warp][q][wl] & below);
+                }
+                // warp exclusive scan of (quads << 16 | degree)
+                const uint32_t packed = ((uint32_t)__popc(qb) << 16) | deg;
+                uint32_t x = packed;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) { const uint32_t y = __shfl_up_sync(kFull, x, d); if (lane >= d) x += y; }
+                const uint32_t tot = __shfl_sync(kFull, x, 31);
+                const uint32_t ex = x - packed;
+                if (act) {
+                    a.points[3 * (int64_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
+                    a.points[3 * (int64_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
+                    a.points[3 * (int64_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
+                    if (own) {
+                        const uint32_t o = wi - (uint32_t)halo_lo;
+                        uint32_t ss = sbase + run_s + (ex & 0xffffu);
+                        a.fmask[o] = (uint8_t)fm;
+                        a.csr_off[o] = a.first_stencil + ss;
+                        if (fm & 1u) a.csr_ids[ss++] = gn[1];      // -z  (j, k-1)
+                        if (fm & 2u) a.csr_ids[ss++] = gn[2];      // -y  (j-1, k)
+                        if (fm & 4u) a.csr_ids[ss++] = g - 1u;     // -x
+                        if (fm & 8u) a.csr_ids[ss++] = g + 1u;     // +x
+                        if (fm & 16u) a.csr_ids[ss++] = gn[3];     // +y  (j+1, k)
+                        if (fm & 32u) a.csr_ids[ss++] = gn[4];     // +z  (j, k+1)
+                        uint32_t qs = qbase + run_q + (ex >> 16);
+                        if (qb & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
+                            *reinterpret_cast<uint4 *>(a.quads + 4 * (int64_t)qs) = make_uint4(gn[0], gn[1], g, gn[2]);
+                            *reinterpret_cast<uint2 *>(a.pairs + 2 * (int64_t)qs) = make_uint2(cA, cA1);
+                            ++qs;
+                        }
+                        if (qb & 2u) {   // y-quad [(i-1,k-1), (i-1,k), (i,k), (i,k-1)] of row j
+                            *reinterpret_cast<uint4 *>(a.quads + 4 * (int64_t)qs) = make_uint4(gn[1] - 1u, g - 1u, g, gn[1]);
+                            *reinterpret_cast<uint2 *>(a.pairs + 2 * (int64_t)qs) = make_uint2(cA, cB);
+                            ++qs;
+                        }
+                        if (qb & 4u) {   // z-quad [(i-1,j-1), (i,j-1), (i,j), (i-1,j)] of layer k
+                            *reinterpret_cast<uint4 *>(a.quads + 4 * (int64_t)qs) = make_uint4(gn[2] - 1u, gn[2], g, g - 1u);
+                            *reinterpret_cast<uint2 *>(a.pairs + 2 * (int64_t)qs) = make_uint2(cA, cC);
+                            ++qs;
+                        }
+                    }
+                }
+                run_q += tot >> 16;
+                run_s += tot & 0xffffu;
+            }
+            run_o += blk_pts;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) run_n[q] += blk_n[q];
+            __syncwarp();
         }
     }
 }

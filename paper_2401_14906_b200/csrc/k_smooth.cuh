@@ -45,33 +45,28 @@ __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_own;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t w = a.halo_lo + i;
+        const uint32_t f = a.fmask[i];
         float ox = 0.f, oy = 0.f, oz = 0.f;
         if (a.src) { ox = a.src[3 * w]; oy = a.src[3 * w + 1]; oz = a.src[3 * w + 2]; }
-        uint32_t f = a.fmask[i];
         float nx = ox, ny = oy, nz = oz;
         if (f) {
             const uint32_t s0 = a.csr_off[i] - a.first_stencil;
-            float sx = 0.f, sy = 0.f, sz = 0.f;
-            int n = 0;
-            while (f) {
-                const int face = __ffs(f) - 1;
-                f &= f - 1;
-                const int64_t wj = (int64_t)(a.csr_ids[s0 + n] - a.win_base);
-                ++n;
-                float dx = 0.f, dy = 0.f, dz = 0.f;
-                if (a.src) { dx = a.src[3 * wj] - ox; dy = a.src[3 * wj + 1] - oy; dz = a.src[3 * wj + 2] - oz; }
-                // e_f: faces -z,-y,-x,+x,+y,+z
-                switch (face) {
-                    case 0: dz -= 1.f; break;
-                    case 1: dy -= 1.f; break;
-                    case 2: dx -= 1.f; break;
-                    case 3: dx += 1.f; break;
-                    case 4: dy += 1.f; break;
-                    default: dz += 1.f; break;
+            const int deg = __popc(f);
+            // sum_j (e_f + o_j - o_i) = e + sum_j o_j - deg * o_i, with e the sum of the
+            // face directions: faces -z,-y,-x,+x,+y,+z are mask bits 0..5
+            float sx = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
+            float sy = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
+            float sz = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
+            if (a.src) {
+                float ax = 0.f, ay = 0.f, az = 0.f;
+                for (int n = 0; n < deg; ++n) {
+                    const uint32_t wj = a.csr_ids[s0 + n] - a.win_base;
+                    ax += a.src[3 * (size_t)wj]; ay += a.src[3 * (size_t)wj + 1]; az += a.src[3 * (size_t)wj + 2];
                 }
-                sx += dx; sy += dy; sz += dz;
+                const float fd = (float)deg;
+                sx += ax - fd * ox; sy += ay - fd * oy; sz += az - fd * oz;
             }
-            const float fn = (float)n;   // m = sum / N, q = o + lambda * m, clamp (readings Q8, Q9)
+            const float fn = (float)deg;   // m = sum / N, q = o + lambda * m, clamp (readings Q8, Q9)
             nx = fminf(fmaxf(__fadd_rn(ox, __fmul_rn(a.lambda, __fdiv_rn(sx, fn))), -a.d), a.d);
             ny = fminf(fmaxf(__fadd_rn(oy, __fmul_rn(a.lambda, __fdiv_rn(sy, fn))), -a.d), a.d);
             nz = fminf(fmaxf(__fadd_rn(oz, __fmul_rn(a.lambda, __fdiv_rn(sz, fn))), -a.d), a.d);

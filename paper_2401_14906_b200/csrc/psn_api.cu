@@ -56,9 +56,10 @@ psn_status cuda_check(psn_ctx *ctx, const char *where) {
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 
 struct Layout {
-    int64_t M, N, O, kA, kB, R, W4, nTiles;
+    int64_t M, N, O, kA, kB, R, W32, nTiles;
     size_t hdr, tiles, cntP, cntQ, cntS, offP, offQ, offS, trim, pmask, labels, total;
 };
 
@@ -83,7 +84,7 @@ psn_status layout(psn_ctx *ctx, const psn_volume *v, Layout *L) {
         return fail(ctx, PSN_ERR_ARG, "slab slices [%lld,%lld) must contain [%lld,%lld] (one-slice halos)",
                     (long long)v->z_lo, (long long)v->z_hi, (long long)L->kA, (long long)L->kB);
     L->R = (N - 1) * (L->kB - L->kA);
-    L->W4 = (M - 1 + 127) / 128;
+    L->W32 = (M - 1 + 31) / 32;
     L->nTiles = (L->R + kScanTile - 1) / kScanTile;
     size_t off = 0;
     L->hdr = off; off += align_up(sizeof(ScanHeader));
@@ -95,7 +96,7 @@ psn_status layout(psn_ctx *ctx, const psn_volume *v, Layout *L) {
     L->offQ = off; off += align_up(4 * (size_t)L->R);
     L->offS = off; off += align_up(4 * (size_t)L->R);
     L->trim = off; off += align_up(8 * (size_t)L->R);
-    L->pmask = off; off += align_up(16 * (size_t)L->R * (size_t)L->W4);
+    L->pmask = off; off += align_up(4 * (size_t)L->R * (size_t)L->W32);
     L->labels = off;
     off += align_up(v->dtype == PSN_U32 ? 4 * (size_t)kMaxList : 8192);
     L->total = off;
@@ -148,25 +149,28 @@ __global__ void k_init_multixt(uint32_t *cp, uint32_t *cq, uint32_t *cs, int2 *t
     }
 }
 
-template <typename T, bool ANZ, bool VEC>
-void launch_count(const CountArgs &ca, int64_t blocks, int threads, cudaStream_t st) {
-    constexpr int TJ = sizeof(T) == 1 ? 8 : (sizeof(T) == 2 ? 4 : 2);
-    k_count<T, TJ, ANZ, VEC><<<(unsigned)blocks, threads, 0, st>>>(ca);
+template <typename T, bool ANZ>
+cudaError_t launch_count(const CountArgs &ca, int64_t blocks, int threads, size_t smem, cudaStream_t st) {
+    constexpr int TJ = count_tj<T>();
+    static bool attr_set = false;   // one-time opt-in to >48 KB dynamic shared memory
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_count<T, TJ, ANZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    k_count<T, TJ, ANZ><<<(unsigned)blocks, threads, smem, st>>>(ca);
+    return cudaGetLastError();
 }
 
 template <typename T>
-int tj_of() { return sizeof(T) == 1 ? 8 : (sizeof(T) == 2 ? 4 : 2); }
-
-template <typename T>
-void dispatch_count(const CountArgs &ca, bool anz, bool vec, int64_t blocks, int threads, cudaStream_t st) {
-    if (anz) { if (vec) launch_count<T, true, true>(ca, blocks, threads, st); else launch_count<T, true, false>(ca, blocks, threads, st); }
-    else     { if (vec) launch_count<T, false, true>(ca, blocks, threads, st); else launch_count<T, false, false>(ca, blocks, threads, st); }
+cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int threads, size_t smem, cudaStream_t st) {
+    return anz ? launch_count<T, true>(ca, blocks, threads, smem, st) : launch_count<T, false>(ca, blocks, threads, smem, st);
 }
 
 template <typename T>
-void dispatch_emit(const EmitArgs &ea, bool anz, bool vec, int64_t blocks, cudaStream_t st) {
-    if (anz) { if (vec) k_emit<T, true, true><<<(unsigned)blocks, 256, 0, st>>>(ea); else k_emit<T, true, false><<<(unsigned)blocks, 256, 0, st>>>(ea); }
-    else     { if (vec) k_emit<T, false, true><<<(unsigned)blocks, 256, 0, st>>>(ea); else k_emit<T, false, false><<<(unsigned)blocks, 256, 0, st>>>(ea); }
+void dispatch_emit(const EmitArgs &ea, bool anz, int64_t blocks, cudaStream_t st) {
+    if (anz) k_emit<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
+    else k_emit<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
 }
 
 void signature(const psn_volume *v, int64_t sig[6]) {
@@ -257,7 +261,6 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int eb = (int)vol->dtype;
-    const bool vec = (L.M % 4 == 0) && ((reinterpret_cast<uintptr_t>(vol->labels) & 15u) == 0);
     LabelSet ls;
     bool anz = true;
     s = prepare_labels(ctx, vol, labels, ws, L, st, &ls, &anz);
@@ -266,23 +269,30 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
 
     if (phase & PSN_COUNT) {
         if (cudaMemsetAsync(at<char>(ws, L.hdr), 0, L.cntP - L.hdr, st) != cudaSuccess) return cuda_check(ctx, "memset");
-        const int64_t nXT = (L.W4 + 7) / 8;
-        const int64_t WX = std::min<int64_t>(L.W4, 8);
-        const int tj = eb == 1 ? tj_of<uint8_t>() : (eb == 2 ? tj_of<uint16_t>() : tj_of<uint32_t>());
+        const int64_t chunks = (L.M - 1 + 3) / 4;            // 4-voxel lane chunks per row
+        const int64_t nXT = (chunks + 255) / 256;             // 1024 x-positions per CTA
+        const int64_t WX = std::min<int64_t>((chunks + 31) / 32, 8);
+        const int tj = eb == 1 ? count_tj<uint8_t>() : (eb == 2 ? count_tj<uint16_t>() : count_tj<uint32_t>());
         const int64_t nJB = (L.N - 1 + tj - 1) / tj;
         const int64_t nLay = L.kB - L.kA;
-        const int64_t target_warps = (int64_t)ctx->sms * 48;
+        const int64_t target_warps = (int64_t)ctx->sms * 32;
         int64_t nZC = std::max<int64_t>(1, (target_warps + nXT * nJB * WX - 1) / (nXT * nJB * WX));
         nZC = std::min(nZC, nLay);
         const int64_t KZ = (nLay + nZC - 1) / nZC;
         nZC = (nLay + KZ - 1) / KZ;
+        const int64_t xpad = 16 / eb;
+        // every thread of the CTA reads its 4-element chunk and the next word, so a staged row
+        // spans the CTA's full width (zero-filled past the row end), plus the 16-byte pad
+        const int64_t RB = (int64_t)align16((size_t)((128 * WX + xpad) * eb));
+        const size_t smem = (size_t)kCountStages * (size_t)(tj + 1) * (size_t)RB;
         CountArgs ca;
         ca.labels = slab0; ca.M = L.M; ca.N = L.N; ca.O = L.O; ca.z_lo = vol->z_lo;
-        ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W4 = L.W4;
-        ca.nXT = nXT; ca.nJB = nJB; ca.KZ = KZ;
+        ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W32 = L.W32;
+        ca.nXT = nXT; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB;
         ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
         ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask);
         ca.ls = ls; ca.multi_xt = nXT > 1 ? 1 : 0;
+        ca.tma = ((L.M * eb) % 16 == 0) && ((reinterpret_cast<uintptr_t>(slab0) & 15u) == 0);
         const int64_t gridR = std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8);
         if (ca.multi_xt) {
             k_init_multixt<<<(unsigned)gridR, 256, 0, st>>>(ca.cntP, ca.cntQ, ca.cntS, ca.trim, L.R);
@@ -290,9 +300,11 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         }
         const int64_t blocks = nXT * nJB * nZC;
         const int threads = (int)(32 * WX);
-        if (eb == 1) dispatch_count<uint8_t>(ca, anz, vec, blocks, threads, st);
-        else if (eb == 2) dispatch_count<uint16_t>(ca, anz, vec, blocks, threads, st);
-        else dispatch_count<uint32_t>(ca, anz, vec, blocks, threads, st);
+        cudaError_t ce;
+        if (eb == 1) ce = dispatch_count<uint8_t>(ca, anz, blocks, threads, smem, st);
+        else if (eb == 2) ce = dispatch_count<uint16_t>(ca, anz, blocks, threads, smem, st);
+        else ce = dispatch_count<uint32_t>(ca, anz, blocks, threads, smem, st);
+        if (ce != cudaSuccess) return fail(ctx, PSN_ERR_CUDA, "k_count launch: %s", cudaGetErrorString(ce));
         ++ctx->launches;
         if (ca.multi_xt) {
             k_trim_fix<<<(unsigned)gridR, 256, 0, st>>>(ca.trim, ca.cntP, L.R);
@@ -329,7 +341,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         return fail(ctx, PSN_ERR_ARG, "quads must be 16-byte and pairs 8-byte aligned");
     EmitArgs ea;
     ea.labels = slab0; ea.M = L.M; ea.N = L.N; ea.O = L.O; ea.z_lo = vol->z_lo;
-    ea.kA = L.kA; ea.kB = L.kB; ea.own_k0 = vol->own_k0; ea.own_k1 = vol->own_k1; ea.W4 = L.W4; ea.R = L.R;
+    ea.kA = L.kA; ea.kB = L.kB; ea.own_k0 = vol->own_k0; ea.own_k1 = vol->own_k1; ea.W32 = L.W32; ea.R = L.R;
     ea.cntP = at<uint32_t>(ws, L.cntP); ea.offP = at<uint32_t>(ws, L.offP);
     ea.offQ = at<uint32_t>(ws, L.offQ); ea.offS = at<uint32_t>(ws, L.offS); ea.pmask = at<uint32_t>(ws, L.pmask);
     ea.ls = ls;
@@ -341,9 +353,9 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.first_stencil = (uint32_t)mesh->first_stencil;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
-    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, vec, blocks, st);
-    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, vec, blocks, st);
-    else dispatch_emit<uint32_t>(ea, anz, vec, blocks, st);
+    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, blocks, st);
+    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, blocks, st);
+    else dispatch_emit<uint32_t>(ea, anz, blocks, st);
     ++ctx->launches;
     return cuda_check(ctx, "emit launch");
 }

@@ -321,3 +321,85 @@ class PSN:
 def to_numpy_u32(t: torch.Tensor, n_rows: int):
     """Device int32 view -> host numpy uint32 (first n_rows rows)."""
     return t[:n_rows].cpu().numpy().view("uint32")
+
+
+class Pipeline:
+    """Steady-state extract + smooth (+ triangulate) on one resident volume.
+
+    Buffers are sized once from a two-phase warm-up extraction (COUNT ->
+    allocate -> EMIT); every later run() is PSN_COUNT|PSN_EMIT with those
+    capacities (no host synchronisation) followed by psn_smooth.
+    """
+
+    def __init__(self, psn: PSN, vol: Volume, iterations: int, relaxation: float, constraint: float,
+                 label_set=None, triangulate: bool = False, headroom: float = 0.0):
+        self.psn, self.vol = psn, vol
+        self.T, self.lam, self.d = iterations, relaxation, constraint
+        self.labels = psn.labels(label_set)
+        self.ws = psn.workspace(vol)
+        m0 = psn.extract(vol, label_set, ws=self.ws)
+        self.counts = (m0.n_points, m0.n_quads, m0.n_stencil)
+        h = 1.0 + headroom
+        self.mesh = psn.alloc_mesh(int(m0.n_window * h) + 1, int(m0.n_points * h) + 1,
+                                   int(m0.n_quads * h) + 1, int(m0.n_stencil * h) + 1)
+        self.mesh.c = MeshC.from_buffer_copy(m0.c)
+        self.sws = psn.smooth_workspace(self.mesh.points.shape[0])
+        self.out = torch.empty_like(self.mesh.points)
+        self.tris = torch.empty((max(2 * self.mesh.quads.shape[0], 1), 3), dtype=torch.int32,
+                                device=self.out.device) if triangulate else None
+        self.launches = {}
+
+    def extract(self, stream=None):
+        self.psn.extract_into(self.vol, self.labels, self.ws, self.mesh, stream)
+        # the totals are those of the warm-up volume (same volume every run)
+        self.mesh.c.n_points, self.mesh.c.n_quads, self.mesh.c.n_stencil = self.counts
+        self.launches["extract"] = self.psn.launches
+
+    def smooth(self, stream=None):
+        self.psn.smooth(self.vol, self.mesh, self.T, self.lam, self.d, out=self.out, ws=self.sws, stream=stream)
+        self.launches["smooth"] = self.psn.launches
+        if self.tris is not None:
+            self.psn.triangulate(self.mesh, self.out, out=self.tris, stream=stream)
+            self.launches["triangulate"] = self.psn.launches
+
+    def run(self, stream=None):
+        self.extract(stream)
+        self.smooth(stream)
+
+    def check(self, stream=None):
+        """Synchronising read of the device totals / status of the last run."""
+        self.psn.totals(self.vol, self.ws, self.mesh, stream)
+        return (self.mesh.n_points, self.mesh.n_quads, self.mesh.n_stencil) == self.counts
+
+
+def surface_nets_host(psn: PSN, labels_host: torch.Tensor, spacing, iterations: int, relaxation: float,
+                      constraint: float, origin=(0.0, 0.0, 0.0), label_set=None, state: dict | None = None,
+                      stream=None):
+    """Public end-to-end call with HOST buffers: H2D copy of the label volume
+    (pinned host tensor), extraction + smoothing on the device, D2H copy of the
+    smoothed points, quads and two-tuples into pinned host tensors.  `state`
+    caches device buffers across calls (pass the same dict each time)."""
+    state = {} if state is None else state
+    dev = f"cuda:{psn.device}"
+    if "labels" not in state:
+        state["labels"] = torch.empty(labels_host.shape, dtype=labels_host.dtype, device=dev)
+    lab = state["labels"]
+    lab.copy_(labels_host, non_blocking=True)
+    vol = psn.volume(lab, spacing=spacing, origin=origin)
+    if "pipe" not in state:
+        state["pipe"] = Pipeline(psn, vol, iterations, relaxation, constraint, label_set)
+        pipe = state["pipe"]
+        P, Q = pipe.counts[0], pipe.counts[1]
+        state["h_points"] = torch.empty((P, 3), dtype=torch.float32, pin_memory=True)
+        state["h_quads"] = torch.empty((Q, 4), dtype=torch.int32, pin_memory=True)
+        state["h_pairs"] = torch.empty((Q, 2), dtype=torch.int32, pin_memory=True)
+    pipe = state["pipe"]
+    pipe.vol = vol
+    pipe.run(stream)
+    P, Q = pipe.counts[0], pipe.counts[1]
+    state["h_points"].copy_(pipe.out[:P], non_blocking=True)
+    state["h_quads"].copy_(pipe.mesh.quads[:Q], non_blocking=True)
+    state["h_pairs"].copy_(pipe.mesh.pairs[:Q], non_blocking=True)
+    state["h2d_bytes"] = labels_host.numel() * labels_host.element_size()
+    state["d2h_bytes"] = P * 12 + Q * 24
+    return state["h_points"], state["h_quads"], state["h_pairs"]
