@@ -150,19 +150,28 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
 psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh,
                            const void *ws, size_t ws_bytes, void *stream);
 
-/* Workspace of psn_smooth: two fp32 [n_window][3] index-space offset buffers. */
-psn_status psn_smooth_workspace(int64_t n_points_window, size_t *bytes);
+/* Workspace of the smoothing calls: the smoothing cache (the
+ * extracted mesh is kept so re-smoothing skips re-extraction) -- a fixed-stride
+ * uint32[P][4] table of each own point's -z,-y,+y,+z neighbour window indices
+ * -- followed by two fp32 [n_window][3] index-space offset buffers (used by
+ * psn_smooth's double buffering). */
+psn_status psn_smooth_workspace(const psn_mesh *mesh, size_t *bytes);
+
+/* Build the smoothing cache of `mesh` into ws (psn_smooth does this itself;
+ * slab users call it once before their psn_smooth_step loop). */
+psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_mesh *mesh, void *ws, size_t ws_bytes, void *stream);
 
 /*
  * Constrained Laplacian smoothing (Eq. 1) with double buffering
- * (P:94), `iterations` Jacobi steps on the caller's stream, then world
- * coordinates of every window point into out[w][3]:
+ * (P:94): builds the smoothing cache, runs `iterations` Jacobi steps on the
+ * caller's stream, and writes world coordinates of every own point to out[w][3]:
  *   per own point with N = deg > 0:  o' = clamp(o + lambda * mean_j(p_j - p_i)/s, -d, +d)
  * computed on fp32 index-space offsets o from the exact voxel-centre anchor;
  * out = fl32(anchor64 + s * o).  iterations = 0 or lambda = 0 gives the anchors.
  * Single GPU / whole volume only (halo layers empty); a slab uses
- * psn_smooth_step below.  constraint_distance d is in voxel units (box
- * half-width d*s per axis, readings Q9/Q10).
+ * psn_smooth_prepare + psn_smooth_step with a halo exchange between steps.
+ * constraint_distance d is in voxel units (box half-width d*s per axis,
+ * readings Q9/Q10).
  */
 psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, float *out,
                       int32_t iterations, float relaxation, float constraint_distance,
@@ -171,12 +180,12 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
 /*
  * One Jacobi iteration over the own points of a slab: reads the window offset
  * buffer src[n_window][3] (halo entries must hold the neighbours' current
- * values), writes the own entries of dst.  Between steps the caller exchanges
- * the boundary layers (multi-GPU).  src == NULL means "all offsets zero"
- * (first iteration from the anchors).
+ * values), writes the own entries of dst.  ws must hold the smoothing cache
+ * built by psn_smooth_prepare.  src == NULL means "all offsets zero" (first
+ * iteration from the anchors).
  */
-psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const float *src, float *dst,
-                           float relaxation, float constraint_distance, void *stream);
+psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, const float *src,
+                           float *dst, float relaxation, float constraint_distance, void *stream);
 
 /* World coordinates of window entries [w0, w1) from offsets (NULL = anchors). */
 psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,

@@ -21,13 +21,10 @@ struct SmoothArgs {
     float *dst;                // window offsets (own entries written)
     float *world;              // if non-NULL: write world coordinates here instead of dst
     const uint8_t *fmask;      // own points
-    const uint32_t *csr_off;   // own points (global values)
-    const uint32_t *csr_ids;   // global ids
+    const uint4 *nbr;          // own points: window indices of the -z,-y,+y,+z neighbours (k_smooth_prep)
     const float *points;       // window anchors (fp32 voxel centres), for the world output
     int64_t n_own;
     uint32_t halo_lo;          // window index of the first own point
-    uint32_t win_base;         // global id of window index 0
-    uint32_t first_stencil;
     float lambda, d;
     double sp[3], org[3];
 };
@@ -41,42 +38,87 @@ __device__ __forceinline__ float world_of(float p, float o, double org, double s
     return __double2float_rn(__dadd_rn(anchor64_from(p, org, sp), __dmul_rn(sp, (double)o)));
 }
 
+// Smoothing cache: from the CSR stencil, a fixed-stride table of
+// the -z,-y,+y,+z neighbour WINDOW indices of every own point (slots of absent
+// faces hold the point itself).  The +-x neighbours need no table: ids are
+// row-major, so they are w-1 / w+1 (reading Q4).  Built once per psn_smooth.
+__global__ void __launch_bounds__(256) k_smooth_prep(const uint8_t *fmask, const uint32_t *csr_off,
+                                                     const uint32_t *csr_ids, uint4 *nbr, int64_t n_own,
+                                                     uint32_t halo_lo, uint32_t win_base, uint32_t first_stencil) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_own; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = fmask[i];
+        const uint32_t w = halo_lo + (uint32_t)i;
+        uint32_t s = csr_off[i] - first_stencil;
+        uint4 v = make_uint4(w, w, w, w);
+        if (f & 1u) v.x = csr_ids[s++] - win_base;    // -z
+        if (f & 2u) v.y = csr_ids[s++] - win_base;    // -y
+        if (f & 4u) ++s;                              // -x  (w - 1)
+        if (f & 8u) ++s;                              // +x  (w + 1)
+        if (f & 16u) v.z = csr_ids[s++] - win_base;   // +y
+        if (f & 32u) v.w = csr_ids[s++] - win_base;   // +z
+        nbr[i] = v;
+    }
+}
+
+// One Jacobi step of Eq. 1 on index-space offsets (see header comment).
+// Lanes hold consecutive points, so the +-x neighbours (w-1, w+1) come from
+// the adjacent lanes by shuffle; the y/z neighbours are gathered through the
+// smoothing cache.  sum_j (e_f + o_j - o_i) = e + sum_j o_j - deg * o_i.
 __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_own;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t w = a.halo_lo + i;
-        const uint32_t f = a.fmask[i];
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // all lanes of a warp iterate together (shuffles below need full warps)
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < a.n_own; base += stride) {
+        const int64_t i = base + lane;
+        const bool act = i < a.n_own;
+        const uint32_t w = a.halo_lo + (uint32_t)(act ? i : a.n_own - 1);
+        const uint32_t f = act ? a.fmask[i] : 0u;
         float ox = 0.f, oy = 0.f, oz = 0.f;
-        if (a.src) { ox = a.src[3 * w]; oy = a.src[3 * w + 1]; oz = a.src[3 * w + 2]; }
+        uint4 nb = make_uint4(w, w, w, w);
+        if (act) {
+            if (a.src) { ox = a.src[3 * (size_t)w]; oy = a.src[3 * (size_t)w + 1]; oz = a.src[3 * (size_t)w + 2]; }
+            if (f & 0x33u) nb = a.nbr[i];
+        }
+        // +-x neighbours from the adjacent lanes (lane 0 / 31 and the last point load)
+        float mx = __shfl_up_sync(kFull, ox, 1), my = __shfl_up_sync(kFull, oy, 1), mz = __shfl_up_sync(kFull, oz, 1);
+        float px = __shfl_down_sync(kFull, ox, 1), py = __shfl_down_sync(kFull, oy, 1), pz = __shfl_down_sync(kFull, oz, 1);
+        if (!act) continue;
+        const int deg = __popc(f);
         float nx = ox, ny = oy, nz = oz;
-        if (f) {
-            const uint32_t s0 = a.csr_off[i] - a.first_stencil;
-            const int deg = __popc(f);
-            // sum_j (e_f + o_j - o_i) = e + sum_j o_j - deg * o_i, with e the sum of the
-            // face directions: faces -z,-y,-x,+x,+y,+z are mask bits 0..5
+        if (deg) {
             float sx = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
             float sy = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
             float sz = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
             if (a.src) {
                 float ax = 0.f, ay = 0.f, az = 0.f;
-                for (int n = 0; n < deg; ++n) {
-                    const uint32_t wj = a.csr_ids[s0 + n] - a.win_base;
-                    ax += a.src[3 * (size_t)wj]; ay += a.src[3 * (size_t)wj + 1]; az += a.src[3 * (size_t)wj + 2];
+                if (f & 4u) {
+                    if (lane == 0) { mx = a.src[3 * (size_t)(w - 1)]; my = a.src[3 * (size_t)(w - 1) + 1]; mz = a.src[3 * (size_t)(w - 1) + 2]; }
+                    ax += mx; ay += my; az += mz;
                 }
+                if (f & 8u) {
+                    if (lane == 31 || i + 1 >= a.n_own) { px = a.src[3 * (size_t)(w + 1)]; py = a.src[3 * (size_t)(w + 1) + 1]; pz = a.src[3 * (size_t)(w + 1) + 2]; }
+                    ax += px; ay += py; az += pz;
+                }
+                if (f & 1u) { ax += a.src[3 * (size_t)nb.x]; ay += a.src[3 * (size_t)nb.x + 1]; az += a.src[3 * (size_t)nb.x + 2]; }
+                if (f & 2u) { ax += a.src[3 * (size_t)nb.y]; ay += a.src[3 * (size_t)nb.y + 1]; az += a.src[3 * (size_t)nb.y + 2]; }
+                if (f & 16u) { ax += a.src[3 * (size_t)nb.z]; ay += a.src[3 * (size_t)nb.z + 1]; az += a.src[3 * (size_t)nb.z + 2]; }
+                if (f & 32u) { ax += a.src[3 * (size_t)nb.w]; ay += a.src[3 * (size_t)nb.w + 1]; az += a.src[3 * (size_t)nb.w + 2]; }
                 const float fd = (float)deg;
                 sx += ax - fd * ox; sy += ay - fd * oy; sz += az - fd * oz;
             }
-            const float fn = (float)deg;   // m = sum / N, q = o + lambda * m, clamp (readings Q8, Q9)
-            nx = fminf(fmaxf(__fadd_rn(ox, __fmul_rn(a.lambda, __fdiv_rn(sx, fn))), -a.d), a.d);
-            ny = fminf(fmaxf(__fadd_rn(oy, __fmul_rn(a.lambda, __fdiv_rn(sy, fn))), -a.d), a.d);
-            nz = fminf(fmaxf(__fadd_rn(oz, __fmul_rn(a.lambda, __fdiv_rn(sz, fn))), -a.d), a.d);
+            // m = sum / N (N <= 6: multiply by the fp32 reciprocal), q = o + lambda m, clamp (Q8, Q9)
+            const float inv = deg == 1 ? 1.f : deg == 2 ? 0.5f : deg == 3 ? (1.f / 3.f) : deg == 4 ? 0.25f
+                            : deg == 5 ? 0.2f : (1.f / 6.f);
+            nx = fminf(fmaxf(__fadd_rn(ox, __fmul_rn(a.lambda, __fmul_rn(sx, inv))), -a.d), a.d);
+            ny = fminf(fmaxf(__fadd_rn(oy, __fmul_rn(a.lambda, __fmul_rn(sy, inv))), -a.d), a.d);
+            nz = fminf(fmaxf(__fadd_rn(oz, __fmul_rn(a.lambda, __fmul_rn(sz, inv))), -a.d), a.d);
         }
         if (a.world) {
-            a.world[3 * w + 0] = world_of(a.points[3 * w + 0], nx, a.org[0], a.sp[0]);
-            a.world[3 * w + 1] = world_of(a.points[3 * w + 1], ny, a.org[1], a.sp[1]);
-            a.world[3 * w + 2] = world_of(a.points[3 * w + 2], nz, a.org[2], a.sp[2]);
+            a.world[3 * (size_t)w + 0] = world_of(a.points[3 * (size_t)w + 0], nx, a.org[0], a.sp[0]);
+            a.world[3 * (size_t)w + 1] = world_of(a.points[3 * (size_t)w + 1], ny, a.org[1], a.sp[1]);
+            a.world[3 * (size_t)w + 2] = world_of(a.points[3 * (size_t)w + 2], nz, a.org[2], a.sp[2]);
         } else {
-            a.dst[3 * w + 0] = nx; a.dst[3 * w + 1] = ny; a.dst[3 * w + 2] = nz;
+            a.dst[3 * (size_t)w + 0] = nx; a.dst[3 * (size_t)w + 1] = ny; a.dst[3 * (size_t)w + 2] = nz;
         }
     }
 }

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -30,8 +32,8 @@ struct psn_ctx {
     std::string err;
     int64_t launches = 0;
     std::vector<uint32_t> label_host;     // bitset or sorted list kept alive for async copies
-    const void *counted_ws = nullptr;     // workspace holding a valid COUNT result
-    int64_t counted_sig[6] = {0, 0, 0, 0, 0, 0};
+    // workspaces holding a valid COUNT result, with the volume signature they were counted for
+    std::map<const void *, std::array<int64_t, 6>> counted;
 };
 
 namespace {
@@ -173,9 +175,8 @@ void dispatch_emit(const EmitArgs &ea, bool anz, int64_t blocks, cudaStream_t st
     else k_emit<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
 }
 
-void signature(const psn_volume *v, int64_t sig[6]) {
-    sig[0] = v->dims[0]; sig[1] = v->dims[1]; sig[2] = v->dims[2];
-    sig[3] = v->own_k0; sig[4] = v->own_k1; sig[5] = (int64_t)(intptr_t)v->labels;
+std::array<int64_t, 6> signature(const psn_volume *v) {
+    return {v->dims[0], v->dims[1], v->dims[2], v->own_k0, v->own_k1, (int64_t)(intptr_t)v->labels};
 }
 
 psn_status read_totals(psn_ctx *ctx, const psn_volume *v, const Layout &L, const void *ws, psn_mesh *mesh,
@@ -320,13 +321,11 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         k_scan<<<(unsigned)L.nTiles, kScanThreads, 0, st>>>(sa);
         ++ctx->launches;
         if ((s = cuda_check(ctx, "count/scan launch")) != PSN_OK) return s;
-        ctx->counted_ws = ws;
-        signature(vol, ctx->counted_sig);
+        ctx->counted[ws] = signature(vol);
         if (!(phase & PSN_EMIT)) return read_totals(ctx, vol, L, ws, mesh, st, nullptr);
     } else {
-        int64_t sig[6];
-        signature(vol, sig);
-        if (ctx->counted_ws != ws || memcmp(sig, ctx->counted_sig, sizeof(sig)) != 0)
+        auto it = ctx->counted.find(ws);
+        if (it == ctx->counted.end() || it->second != signature(vol))
             return fail(ctx, PSN_ERR_STATE, "PSN_EMIT needs a preceding PSN_COUNT of the same volume on this workspace");
         if (mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points > mesh->cap_points ||
             mesh->n_quads > mesh->cap_quads || mesh->n_stencil > mesh->cap_stencil)
@@ -374,9 +373,22 @@ psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, 
     return PSN_OK;
 }
 
-psn_status psn_smooth_workspace(int64_t n_points_window, size_t *bytes) {
-    if (!bytes || n_points_window < 0) return PSN_ERR_ARG;
-    *bytes = 2 * align_up(12 * (size_t)n_points_window);
+namespace {
+struct SmoothLayout { size_t nbr, buf0, buf1, total; int64_t nw; };
+SmoothLayout smooth_layout(const psn_mesh *m) {
+    SmoothLayout L;
+    L.nw = m->halo_lo_points + m->n_points + m->halo_hi_points;
+    L.nbr = 0;
+    L.buf0 = align_up(16 * (size_t)std::max<int64_t>(m->n_points, 1));
+    L.buf1 = L.buf0 + align_up(12 * (size_t)std::max<int64_t>(L.nw, 1));
+    L.total = L.buf1 + align_up(12 * (size_t)std::max<int64_t>(L.nw, 1));
+    return L;
+}
+}  // namespace
+
+psn_status psn_smooth_workspace(const psn_mesh *mesh, size_t *bytes) {
+    if (!bytes || !mesh || mesh->n_points < 0 || mesh->halo_lo_points < 0 || mesh->halo_hi_points < 0) return PSN_ERR_ARG;
+    *bytes = smooth_layout(mesh).total;
     return PSN_OK;
 }
 
@@ -392,14 +404,13 @@ psn_status check_smooth_args(psn_ctx *ctx, const psn_mesh *mesh, float relaxatio
     return PSN_OK;
 }
 
-SmoothArgs smooth_args(const psn_mesh *mesh, float lambda, float d) {
+SmoothArgs smooth_args(const psn_mesh *mesh, const void *ws, float lambda, float d) {
     SmoothArgs a;
     memset(&a, 0, sizeof(a));
-    a.fmask = mesh->face_masks; a.csr_off = mesh->stencil_offsets; a.csr_ids = mesh->stencil_ids;
+    a.fmask = mesh->face_masks;
+    a.nbr = static_cast<const uint4 *>(ws);
     a.points = mesh->points; a.n_own = mesh->n_points;
     a.halo_lo = (uint32_t)mesh->halo_lo_points;
-    a.win_base = (uint32_t)(mesh->first_point - mesh->halo_lo_points);
-    a.first_stencil = (uint32_t)mesh->first_stencil;
     a.lambda = lambda; a.d = d;
     return a;
 }
@@ -407,7 +418,27 @@ SmoothArgs smooth_args(const psn_mesh *mesh, float lambda, float d) {
 int64_t grid_for(psn_ctx *ctx, int64_t n) {
     return std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 16));
 }
+
+psn_status launch_prep(psn_ctx *ctx, const psn_mesh *mesh, void *ws, cudaStream_t st) {
+    if (mesh->n_points == 0) return PSN_OK;
+    k_smooth_prep<<<(unsigned)grid_for(ctx, mesh->n_points), 256, 0, st>>>(
+        mesh->face_masks, mesh->stencil_offsets, mesh->stencil_ids, static_cast<uint4 *>(ws), mesh->n_points,
+        (uint32_t)mesh->halo_lo_points, (uint32_t)(mesh->first_point - mesh->halo_lo_points),
+        (uint32_t)mesh->first_stencil);
+    ++ctx->launches;
+    return cuda_check(ctx, "smooth prep launch");
+}
 }  // namespace
+
+psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_mesh *mesh, void *ws, size_t ws_bytes, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    psn_status s = check_smooth_args(ctx, mesh, 0.f, 0.f);
+    if (s != PSN_OK) return s;
+    if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    return launch_prep(ctx, mesh, ws, static_cast<cudaStream_t>(stream));
+}
 
 psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, float *out, int32_t iterations,
                       float relaxation, float constraint_distance, void *ws, size_t ws_bytes, void *stream) {
@@ -419,23 +450,23 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     if (iterations < 0) return fail(ctx, PSN_ERR_ARG, "iterations must be >= 0");
     if (mesh->halo_lo_points || mesh->halo_hi_points)
         return fail(ctx, PSN_ERR_ARG, "psn_smooth needs a whole volume; slabs use psn_smooth_step + halo exchange");
-    const int64_t nw = mesh->n_points;
-    size_t need = 0;
-    psn_smooth_workspace(nw, &need);
-    if (!out || !mesh->points || (iterations > 1 && (!ws || ws_bytes < need)))
-        return fail(ctx, PSN_ERR_ARG, "out/points NULL or workspace too small (need %zu)", need);
+    const SmoothLayout SL = smooth_layout(mesh);
+    if (!out || !mesh->points || !ws || ws_bytes < SL.total)
+        return fail(ctx, PSN_ERR_ARG, "out/points NULL or workspace too small (need %zu)", SL.total);
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t nw = mesh->n_points;
     if (nw == 0) return PSN_OK;
-    float *buf[2] = {static_cast<float *>(ws), ws ? reinterpret_cast<float *>(static_cast<char *>(ws) + need / 2) : nullptr};
     const int64_t g = grid_for(ctx, nw);
-    if (iterations == 0) {
+    if (iterations == 0 || relaxation == 0.f) {
         k_finalize<<<(unsigned)g, 256, 0, st>>>(nullptr, mesh->points, out, 0, nw, vol->spacing[0], vol->spacing[1],
                                                vol->spacing[2], vol->origin[0], vol->origin[1], vol->origin[2]);
         ++ctx->launches;
         return cuda_check(ctx, "finalize launch");
     }
-    SmoothArgs a = smooth_args(mesh, relaxation, constraint_distance);
+    if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
+    float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
+    SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
     for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
     const float *src = nullptr;
     for (int32_t t = 0; t < iterations; ++t) {
@@ -450,16 +481,17 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     return cuda_check(ctx, "smooth launch");
 }
 
-psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const float *src, float *dst, float relaxation,
-                           float constraint_distance, void *stream) {
+psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, const float *src,
+                           float *dst, float relaxation, float constraint_distance, void *stream) {
     if (!ctx) return PSN_ERR_ARG;
     ctx->launches = 0;
     psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
     if (s != PSN_OK) return s;
     if (!dst) return fail(ctx, PSN_ERR_ARG, "dst is NULL");
+    if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
     if (mesh->n_points == 0) return PSN_OK;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
-    SmoothArgs a = smooth_args(mesh, relaxation, constraint_distance);
+    SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
     a.src = src; a.dst = dst; a.world = nullptr;
     k_smooth<<<(unsigned)grid_for(ctx, mesh->n_points), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
     ++ctx->launches;

@@ -117,6 +117,7 @@ class SlabPipeline:
         self.counted = MeshC.from_buffer_copy(self.mesh.c)
         self.plan = halo_plan(self.table, self.rank)
         nw = self.mesh.n_window
+        self.sws = psn.smooth_workspace(self.mesh)
         self.buf = [torch.zeros((max(nw, 1), 3), dtype=torch.float32, device=labels_slab.device) for _ in range(2)]
         self.out = torch.empty((max(nw, 1), 3), dtype=torch.float32, device=labels_slab.device)
 
@@ -131,9 +132,10 @@ class SlabPipeline:
     def smooth(self, stream=None):
         """T Jacobi steps with a halo exchange after each (C2; the last one is C3)."""
         src = None
+        self.psn.smooth_prepare(self.mesh, self.sws, stream)
         for t in range(self.T):
             dst = self.buf[t & 1]
-            self.psn.smooth_step(self.mesh, src, dst, self.lam, self.d, stream)
+            self.psn.smooth_step(self.mesh, self.sws, src, dst, self.lam, self.d, stream)
             halo_exchange(dst, self.plan, self.rank, self.group)
             src = dst
         self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, 0, self.mesh.n_window, stream)

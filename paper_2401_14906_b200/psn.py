@@ -84,12 +84,15 @@ def lib():
         L.psn_extract.restype = ctypes.c_int
         L.psn_mesh_totals.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_mesh_totals.restype = ctypes.c_int
-        L.psn_smooth_workspace.argtypes = [i64, ctypes.POINTER(ctypes.c_size_t)]
+        L.psn_smooth_workspace.argtypes = [ctypes.POINTER(MeshC), ctypes.POINTER(ctypes.c_size_t)]
         L.psn_smooth_workspace.restype = ctypes.c_int
+        L.psn_smooth_prepare.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
+        L.psn_smooth_prepare.restype = ctypes.c_int
         L.psn_smooth.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_int32,
                                  ctypes.c_float, ctypes.c_float, vp, ctypes.c_size_t, vp]
         L.psn_smooth.restype = ctypes.c_int
-        L.psn_smooth_step.argtypes = [vp, ctypes.POINTER(MeshC), vp, vp, ctypes.c_float, ctypes.c_float, vp]
+        L.psn_smooth_step.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp, vp, ctypes.c_float,
+                                      ctypes.c_float, vp]
         L.psn_smooth_step.restype = ctypes.c_int
         L.psn_smooth_finalize.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, i64, i64, vp, vp]
         L.psn_smooth_finalize.restype = ctypes.c_int
@@ -103,7 +106,7 @@ def lib():
 
 EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
             "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
-            "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count"]
+            "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count"]
 
 
 def _ptr(t):
@@ -278,9 +281,9 @@ class PSN:
         return mesh
 
     # ------------------------------------------------------------------ smoothing / triangulation
-    def smooth_workspace(self, n_window) -> torch.Tensor:
+    def smooth_workspace(self, mesh: Mesh) -> torch.Tensor:
         n = ctypes.c_size_t()
-        self._check(self.L.psn_smooth_workspace(int(n_window), ctypes.byref(n)))
+        self._check(self.L.psn_smooth_workspace(ctypes.byref(mesh.c), ctypes.byref(n)))
         return torch.empty(max(n.value, 1), dtype=torch.uint8, device=f"cuda:{self.device}")
 
     def smooth(self, vol: Volume, mesh: Mesh, iterations: int, relaxation: float, constraint: float,
@@ -288,16 +291,19 @@ class PSN:
         if out is None:
             out = torch.empty((max(mesh.n_window, 1), 3), dtype=torch.float32, device=mesh.points.device)
         if ws is None:
-            ws = self.smooth_workspace(mesh.n_window)
+            ws = self.smooth_workspace(mesh)
         rc = self.L.psn_smooth(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(out), int(iterations),
                                float(relaxation), float(constraint), _ptr(ws), ws.numel(), _stream(stream))
         self._check(rc)
         return out
 
-    def smooth_step(self, mesh: Mesh, src: torch.Tensor | None, dst: torch.Tensor, relaxation: float,
-                    constraint: float, stream=None):
-        rc = self.L.psn_smooth_step(self.h, ctypes.byref(mesh.c), _ptr(src), _ptr(dst), float(relaxation),
-                                    float(constraint), _stream(stream))
+    def smooth_prepare(self, mesh: Mesh, ws: torch.Tensor, stream=None):
+        self._check(self.L.psn_smooth_prepare(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _stream(stream)))
+
+    def smooth_step(self, mesh: Mesh, ws: torch.Tensor, src: torch.Tensor | None, dst: torch.Tensor,
+                    relaxation: float, constraint: float, stream=None):
+        rc = self.L.psn_smooth_step(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _ptr(src), _ptr(dst),
+                                    float(relaxation), float(constraint), _stream(stream))
         self._check(rc)
 
     def smooth_finalize(self, vol: Volume, mesh: Mesh, offsets: torch.Tensor | None, out: torch.Tensor,
@@ -343,7 +349,7 @@ class Pipeline:
         self.mesh = psn.alloc_mesh(int(m0.n_window * h) + 1, int(m0.n_points * h) + 1,
                                    int(m0.n_quads * h) + 1, int(m0.n_stencil * h) + 1)
         self.mesh.c = MeshC.from_buffer_copy(m0.c)
-        self.sws = psn.smooth_workspace(self.mesh.points.shape[0])
+        self.sws = psn.smooth_workspace(self.mesh)
         self.out = torch.empty_like(self.mesh.points)
         self.tris = torch.empty((max(2 * self.mesh.quads.shape[0], 1), 3), dtype=torch.int32,
                                 device=self.out.device) if triangulate else None
