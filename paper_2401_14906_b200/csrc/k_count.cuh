@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
     __shared__ uint32_t sP[2][TJ], sQ[2][TJ], sS[2][TJ];
     __shared__ int sL[2][TJ], sR[2][TJ];
     __shared__ uint32_t spm[2][TJ][32];
-    __shared__ uint16_t squeue[8][32 * TJ];
+    __shared__ uint16_t squeue[2 * TJ * 256];   // CTA task queue of a 2-layer batch: (layer bit, row, chunk)
+    __shared__ uint32_t sqn;
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,11 +231,10 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
         }
     };
 
-    auto step = [&](int64_t o, const uint32_t (&Wl)[TJ + 1][NW], uint32_t hul, uint32_t eql,
+    // FAST test of one layer: every thread checks its chunk for the TJ rows and
+    // appends the non-uniform (row, chunk) pairs to the CTA queue.
+    auto fast = [&](int64_t o, const uint32_t (&Wl)[TJ + 1][NW], uint32_t hul, uint32_t eql,
                     const uint32_t (&Wh)[TJ + 1][NW], uint32_t huh, uint32_t eqh) {
-        const int64_t k = kbeg + o;
-        const int slot = (int)(o & 1);
-        const bool own = (k >= a.own_k0) && (k < a.own_k1);
         uint32_t eqz = 0;
 #pragma unroll
         for (int r = 0; r < TJ; ++r) {
@@ -245,7 +245,6 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
         }
         const uint32_t uni = hul & (hul >> 1) & huh & (huh >> 1) & eql & eqh & eqz;
         const uint32_t slow = chunk_has_voxel ? (~uni & rows_valid) : 0u;
-        // compact the slow (row, chunk) tasks of this warp
         const uint32_t cnt = __popc(slow);
         uint32_t incl = cnt;
 #pragma unroll
@@ -255,60 +254,85 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
         }
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         if (total) {
-            uint32_t pos = incl - cnt, m = slow;
+            uint32_t pos = 0;
+            if (lane == 31) pos = atomicAdd(&sqn, total);
+            pos = __shfl_sync(kFull, pos, 31) + incl - cnt;
+            uint32_t m = slow;
+            const uint32_t tag = (uint32_t)(o & 1) << 15 | (uint32_t)tid;
             while (m) {
                 const int r = __ffs(m) - 1;
                 m &= m - 1;
-                squeue[warp][pos++] = (uint16_t)(r * 32 + lane);
-            }
-            __syncwarp();
-            for (uint32_t t = lane; t < total; t += 32) {
-                const uint32_t task = squeue[warp][t];
-                process_task(o, (int)(task >> 5), warp * 32 + (int)(task & 31), k, own, slot);
+                squeue[pos++] = (uint16_t)(tag | (uint32_t)r << 8);
             }
         }
-        __syncthreads();
-        // flush this layer's rows (double-buffered slots: one barrier per layer)
-        for (int t = tid; t < TJ * 32; t += blockDim.x) {
-            const int r = t >> 5, w = t & 31;
-            const int64_t gw = (x_t0 >> 5) + w;
-            if (((rows_valid >> r) & 1u) && gw < a.W32) {
-                const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
-                a.pmask[rr * a.W32 + gw] = spm[slot][r][w];
-            }
-            spm[slot][r][w] = 0u;
-        }
-        if (tid < TJ) {
-            const int r = tid;
-            if ((rows_valid >> r) & 1u) {
-                const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
-                const uint32_t p = sP[slot][r];
-                const int xl = p ? sL[slot][r] : 0, xr = p ? sR[slot][r] + 1 : 0;
-                if (!a.multi_xt) {
-                    a.cntP[rr] = p; a.cntQ[rr] = sQ[slot][r]; a.cntS[rr] = sS[slot][r];
-                    a.trim[rr] = make_int2(xl, xr);
-                } else if (p) {
-                    atomicAdd(&a.cntP[rr], p); atomicAdd(&a.cntQ[rr], sQ[slot][r]);
-                    atomicAdd(&a.cntS[rr], sS[slot][r]);
-                    atomicMin(&a.trim[rr].x, xl); atomicMax(&a.trim[rr].y, xr);
-                }
-            }
-            sP[slot][r] = 0; sQ[slot][r] = 0; sS[slot][r] = 0; sL[slot][r] = 0x7fffffff; sR[slot][r] = -1;
-        }
-        // slice o is no longer read: refill its stage with slice o + NS
-        if (o + NS <= nsteps) fill(o + NS);
     };
 
+    // SLOW phase of a batch of 1-2 layers [o0, o0+nb): all threads drain the
+    // CTA queue with full lanes, then the layers' rows are flushed and their
+    // lower slices released to the TMA producer.
+    auto batch = [&](int64_t o0, int nb) {
+        __syncthreads();
+        const uint32_t nq = sqn;
+        for (uint32_t t = tid; t < nq; t += blockDim.x) {
+            const uint32_t task = squeue[t];
+            const int ob = (int)(task >> 15);
+            const int64_t o = o0 + ob;
+            const int64_t k = kbeg + o;
+            const bool own = (k >= a.own_k0) && (k < a.own_k1);
+            process_task(o, (int)((task >> 8) & 0x7f), (int)(task & 0xff), k, own, (int)(o & 1));
+        }
+        __syncthreads();
+        if (tid == 0) sqn = 0;
+        for (int b = 0; b < nb; ++b) {
+            const int64_t o = o0 + b;
+            const int64_t k = kbeg + o;
+            const int slot = (int)(o & 1);
+            for (int t = tid; t < TJ * 32; t += blockDim.x) {
+                const int r = t >> 5, w = t & 31;
+                const int64_t gw = (x_t0 >> 5) + w;
+                if (((rows_valid >> r) & 1u) && gw < a.W32) {
+                    const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
+                    a.pmask[rr * a.W32 + gw] = spm[slot][r][w];
+                }
+                spm[slot][r][w] = 0u;
+            }
+            if (tid < TJ) {
+                const int r = tid;
+                if ((rows_valid >> r) & 1u) {
+                    const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
+                    const uint32_t p = sP[slot][r];
+                    const int xl = p ? sL[slot][r] : 0, xr = p ? sR[slot][r] + 1 : 0;
+                    if (!a.multi_xt) {
+                        a.cntP[rr] = p; a.cntQ[rr] = sQ[slot][r]; a.cntS[rr] = sS[slot][r];
+                        a.trim[rr] = make_int2(xl, xr);
+                    } else if (p) {
+                        atomicAdd(&a.cntP[rr], p); atomicAdd(&a.cntQ[rr], sQ[slot][r]);
+                        atomicAdd(&a.cntS[rr], sS[slot][r]);
+                        atomicMin(&a.trim[rr].x, xl); atomicMax(&a.trim[rr].y, xr);
+                    }
+                }
+                sP[slot][r] = 0; sQ[slot][r] = 0; sS[slot][r] = 0; sL[slot][r] = 0x7fffffff; sR[slot][r] = -1;
+            }
+            // slice o is no longer read: refill its stage with slice o + NS
+            if (o + NS <= nsteps) fill(o + NS);
+        }
+    };
+
+    if (tid == 0) sqn = 0;
+    __syncthreads();
     wait(0);
     load_flags(0, Wa, huA, eqA);
     for (int64_t o = 0; o < nsteps; o += 2) {
         wait(o + 1);
         load_flags(o + 1, Wb, huB, eqB);
-        step(o, Wa, huA, eqA, Wb, huB, eqB);
-        if (o + 1 >= nsteps) break;
-        wait(o + 2);
-        load_flags(o + 2, Wa, huA, eqA);
-        step(o + 1, Wb, huB, eqB, Wa, huA, eqA);
+        fast(o, Wa, huA, eqA, Wb, huB, eqB);
+        const bool two = o + 1 < nsteps;
+        if (two) {
+            wait(o + 2);
+            load_flags(o + 2, Wa, huA, eqA);
+            fast(o + 1, Wb, huB, eqB, Wa, huA, eqA);
+        }
+        batch(o, two ? 2 : 1);
     }
 }
 

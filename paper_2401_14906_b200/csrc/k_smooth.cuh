@@ -61,64 +61,94 @@ __global__ void __launch_bounds__(256) k_smooth_prep(const uint8_t *fmask, const
 }
 
 // One Jacobi step of Eq. 1 on index-space offsets (see header comment).
-// Lanes hold consecutive points, so the +-x neighbours (w-1, w+1) come from
-// the adjacent lanes by shuffle; the y/z neighbours are gathered through the
-// smoothing cache.  sum_j (e_f + o_j - o_i) = e + sum_j o_j - deg * o_i.
+// A warp owns 64 consecutive points (two per lane, lane and lane+32) so that
+// every load of both points is in flight before any is used.  The +-x
+// neighbours (w-1, w+1) come from the adjacent lanes by shuffle; the y/z
+// neighbours are gathered through the smoothing cache, unconditionally (absent
+// faces point at the point itself, a cache hit) and masked arithmetically.
+// sum_j (e_f + o_j - o_i) = e + sum_j o_j - deg * o_i.
+__device__ __forceinline__ float3 ld3(const float *__restrict__ p, uint32_t w) {
+    return make_float3(__ldg(p + 3u * w), __ldg(p + 3u * w + 1u), __ldg(p + 3u * w + 2u));
+}
+
 __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
     const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // all lanes of a warp iterate together (shuffles below need full warps)
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < a.n_own; base += stride) {
-        const int64_t i = base + lane;
-        const bool act = i < a.n_own;
-        const uint32_t w = a.halo_lo + (uint32_t)(act ? i : a.n_own - 1);
-        const uint32_t f = act ? a.fmask[i] : 0u;
-        float ox = 0.f, oy = 0.f, oz = 0.f;
-        uint4 nb = make_uint4(w, w, w, w);
-        if (act) {
-            if (a.src) { ox = a.src[3 * (size_t)w]; oy = a.src[3 * (size_t)w + 1]; oz = a.src[3 * (size_t)w + 2]; }
-            if (f & 0x33u) nb = a.nbr[i];
+    const float *__restrict__ src = a.src;
+    const uint32_t n = (uint32_t)a.n_own;
+    const uint32_t stride = gridDim.x * (blockDim.x >> 5) * 64u;
+    for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 64u; base < n; base += stride) {
+        uint32_t i[2], w[2], f[2];
+        uint4 nb[2];
+        float3 o[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            i[u] = base + 32u * u + lane;
+            const uint32_t ii = i[u] < n ? i[u] : n - 1u;
+            w[u] = a.halo_lo + ii;
+            f[u] = i[u] < n ? (uint32_t)__ldg(a.fmask + ii) : 0u;
+            nb[u] = __ldg(a.nbr + ii);
+            o[u] = src ? ld3(src, w[u]) : make_float3(0.f, 0.f, 0.f);
         }
-        // +-x neighbours from the adjacent lanes (lane 0 / 31 and the last point load)
-        float mx = __shfl_up_sync(kFull, ox, 1), my = __shfl_up_sync(kFull, oy, 1), mz = __shfl_up_sync(kFull, oz, 1);
-        float px = __shfl_down_sync(kFull, ox, 1), py = __shfl_down_sync(kFull, oy, 1), pz = __shfl_down_sync(kFull, oz, 1);
-        if (!act) continue;
-        const int deg = __popc(f);
-        float nx = ox, ny = oy, nz = oz;
-        if (deg) {
-            float sx = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
-            float sy = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
-            float sz = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
-            if (a.src) {
-                float ax = 0.f, ay = 0.f, az = 0.f;
-                if (f & 4u) {
-                    if (lane == 0) { mx = a.src[3 * (size_t)(w - 1)]; my = a.src[3 * (size_t)(w - 1) + 1]; mz = a.src[3 * (size_t)(w - 1) + 2]; }
-                    ax += mx; ay += my; az += mz;
-                }
-                if (f & 8u) {
-                    if (lane == 31 || i + 1 >= a.n_own) { px = a.src[3 * (size_t)(w + 1)]; py = a.src[3 * (size_t)(w + 1) + 1]; pz = a.src[3 * (size_t)(w + 1) + 2]; }
-                    ax += px; ay += py; az += pz;
-                }
-                if (f & 1u) { ax += a.src[3 * (size_t)nb.x]; ay += a.src[3 * (size_t)nb.x + 1]; az += a.src[3 * (size_t)nb.x + 2]; }
-                if (f & 2u) { ax += a.src[3 * (size_t)nb.y]; ay += a.src[3 * (size_t)nb.y + 1]; az += a.src[3 * (size_t)nb.y + 2]; }
-                if (f & 16u) { ax += a.src[3 * (size_t)nb.z]; ay += a.src[3 * (size_t)nb.z + 1]; az += a.src[3 * (size_t)nb.z + 2]; }
-                if (f & 32u) { ax += a.src[3 * (size_t)nb.w]; ay += a.src[3 * (size_t)nb.w + 1]; az += a.src[3 * (size_t)nb.w + 2]; }
-                const float fd = (float)deg;
-                sx += ax - fd * ox; sy += ay - fd * oy; sz += az - fd * oz;
+        // y/z gathers (all issued before the arithmetic)
+        float3 g[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (src) {
+                g[u][0] = ld3(src, nb[u].x); g[u][1] = ld3(src, nb[u].y);
+                g[u][2] = ld3(src, nb[u].z); g[u][3] = ld3(src, nb[u].w);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) g[u][q] = make_float3(0.f, 0.f, 0.f);
             }
-            // m = sum / N (N <= 6: multiply by the fp32 reciprocal), q = o + lambda m, clamp (Q8, Q9)
-            const float inv = deg == 1 ? 1.f : deg == 2 ? 0.5f : deg == 3 ? (1.f / 3.f) : deg == 4 ? 0.25f
-                            : deg == 5 ? 0.2f : (1.f / 6.f);
-            nx = fminf(fmaxf(__fadd_rn(ox, __fmul_rn(a.lambda, __fmul_rn(sx, inv))), -a.d), a.d);
-            ny = fminf(fmaxf(__fadd_rn(oy, __fmul_rn(a.lambda, __fmul_rn(sy, inv))), -a.d), a.d);
-            nz = fminf(fmaxf(__fadd_rn(oz, __fmul_rn(a.lambda, __fmul_rn(sz, inv))), -a.d), a.d);
         }
-        if (a.world) {
-            a.world[3 * (size_t)w + 0] = world_of(a.points[3 * (size_t)w + 0], nx, a.org[0], a.sp[0]);
-            a.world[3 * (size_t)w + 1] = world_of(a.points[3 * (size_t)w + 1], ny, a.org[1], a.sp[1]);
-            a.world[3 * (size_t)w + 2] = world_of(a.points[3 * (size_t)w + 2], nz, a.org[2], a.sp[2]);
-        } else {
-            a.dst[3 * (size_t)w + 0] = nx; a.dst[3 * (size_t)w + 1] = ny; a.dst[3 * (size_t)w + 2] = nz;
+        // +-x neighbours: lane-1 / lane+1 of the same half; across the halves and the warp ends
+        float3 mxo[2], pxo[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            mxo[u].x = __shfl_up_sync(kFull, o[u].x, 1); mxo[u].y = __shfl_up_sync(kFull, o[u].y, 1);
+            mxo[u].z = __shfl_up_sync(kFull, o[u].z, 1);
+            pxo[u].x = __shfl_down_sync(kFull, o[u].x, 1); pxo[u].y = __shfl_down_sync(kFull, o[u].y, 1);
+            pxo[u].z = __shfl_down_sync(kFull, o[u].z, 1);
+        }
+        {   // lane 31 of half 0 <-> lane 0 of half 1
+            const float bx = __shfl_sync(kFull, o[1].x, 0), by = __shfl_sync(kFull, o[1].y, 0), bz = __shfl_sync(kFull, o[1].z, 0);
+            const float ex = __shfl_sync(kFull, o[0].x, 31), ey = __shfl_sync(kFull, o[0].y, 31), ez = __shfl_sync(kFull, o[0].z, 31);
+            if (lane == 31) pxo[0] = make_float3(bx, by, bz);
+            if (lane == 0) mxo[1] = make_float3(ex, ey, ez);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (i[u] >= n) continue;
+            const uint32_t fu = f[u];
+            float3 r = o[u];
+            if (fu) {
+                if (src) {
+                    if ((fu & 4u) && lane == 0 && u == 0) mxo[0] = ld3(src, w[u] - 1u);
+                    if ((fu & 8u) && (lane == 31 && u == 1 || i[u] + 1u >= n)) pxo[u] = ld3(src, w[u] + 1u);
+                }
+                const float m0 = (fu & 1u) ? 1.f : 0.f, m1 = (fu & 2u) ? 1.f : 0.f, m2 = (fu & 4u) ? 1.f : 0.f;
+                const float m3 = (fu & 8u) ? 1.f : 0.f, m4 = (fu & 16u) ? 1.f : 0.f, m5 = (fu & 32u) ? 1.f : 0.f;
+                const int deg = __popc(fu);
+                const float fd = (float)deg;
+                // e (face directions) + sum of neighbour offsets - deg * o
+                float sx = (m3 - m2) + (m2 * mxo[u].x + m3 * pxo[u].x + m0 * g[u][0].x + m1 * g[u][1].x + m4 * g[u][2].x + m5 * g[u][3].x) - fd * o[u].x;
+                float sy = (m4 - m1) + (m2 * mxo[u].y + m3 * pxo[u].y + m0 * g[u][0].y + m1 * g[u][1].y + m4 * g[u][2].y + m5 * g[u][3].y) - fd * o[u].y;
+                float sz = (m5 - m0) + (m2 * mxo[u].z + m3 * pxo[u].z + m0 * g[u][0].z + m1 * g[u][1].z + m4 * g[u][2].z + m5 * g[u][3].z) - fd * o[u].z;
+                // m = sum / N (N <= 6: multiply by the fp32 reciprocal), q = o + lambda m, clamp (Q8, Q9)
+                const float inv = deg == 1 ? 1.f : deg == 2 ? 0.5f : deg == 3 ? (1.f / 3.f) : deg == 4 ? 0.25f
+                                : deg == 5 ? 0.2f : (1.f / 6.f);
+                r.x = fminf(fmaxf(__fadd_rn(o[u].x, __fmul_rn(a.lambda, __fmul_rn(sx, inv))), -a.d), a.d);
+                r.y = fminf(fmaxf(__fadd_rn(o[u].y, __fmul_rn(a.lambda, __fmul_rn(sy, inv))), -a.d), a.d);
+                r.z = fminf(fmaxf(__fadd_rn(o[u].z, __fmul_rn(a.lambda, __fmul_rn(sz, inv))), -a.d), a.d);
+            }
+            const uint32_t ww = w[u];
+            if (a.world) {
+                a.world[3u * ww + 0u] = world_of(__ldg(a.points + 3u * ww + 0u), r.x, a.org[0], a.sp[0]);
+                a.world[3u * ww + 1u] = world_of(__ldg(a.points + 3u * ww + 1u), r.y, a.org[1], a.sp[1]);
+                a.world[3u * ww + 2u] = world_of(__ldg(a.points + 3u * ww + 2u), r.z, a.org[2], a.sp[2]);
+            } else {
+                a.dst[3u * ww + 0u] = r.x; a.dst[3u * ww + 1u] = r.y; a.dst[3u * ww + 2u] = r.z;
+            }
         }
     }
 }

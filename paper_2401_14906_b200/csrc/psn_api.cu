@@ -154,11 +154,11 @@ __global__ void k_init_multixt(uint32_t *cp, uint32_t *cq, uint32_t *cs, int2 *t
 template <typename T, bool ANZ>
 cudaError_t launch_count(const CountArgs &ca, int64_t blocks, int threads, size_t smem, cudaStream_t st) {
     constexpr int TJ = count_tj<T>();
-    static bool attr_set = false;   // one-time opt-in to >48 KB dynamic shared memory
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_count<T, TJ, ANZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    static size_t attr_set = 0;   // opt-in to > 48 KB dynamic shared memory (largest request so far)
+    if (smem > attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_count<T, TJ, ANZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set = smem;
     }
     k_count<T, TJ, ANZ><<<(unsigned)blocks, threads, smem, st>>>(ca);
     return cudaGetLastError();
@@ -458,6 +458,7 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     const int64_t nw = mesh->n_points;
     if (nw == 0) return PSN_OK;
     const int64_t g = grid_for(ctx, nw);
+    const int64_t gs = std::max<int64_t>(1, std::min<int64_t>((nw + 511) / 512, (int64_t)ctx->sms * 16));  // 64 points per warp
     if (iterations == 0 || relaxation == 0.f) {
         k_finalize<<<(unsigned)g, 256, 0, st>>>(nullptr, mesh->points, out, 0, nw, vol->spacing[0], vol->spacing[1],
                                                vol->spacing[2], vol->origin[0], vol->origin[1], vol->origin[2]);
@@ -474,7 +475,7 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         const bool last = (t == iterations - 1);
         a.dst = last ? nullptr : buf[t & 1];
         a.world = last ? out : nullptr;
-        k_smooth<<<(unsigned)g, 256, 0, st>>>(a);
+        k_smooth<<<(unsigned)gs, 256, 0, st>>>(a);
         ++ctx->launches;
         src = a.dst;
     }
@@ -493,7 +494,8 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, s
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
     a.src = src; a.dst = dst; a.world = nullptr;
-    k_smooth<<<(unsigned)grid_for(ctx, mesh->n_points), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    const int64_t gs = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 511) / 512, (int64_t)ctx->sms * 16));
+    k_smooth<<<(unsigned)gs, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
     ++ctx->launches;
     return cuda_check(ctx, "smooth step launch");
 }
