@@ -5,22 +5,23 @@
 // them into the per-voxel edge case and the point / quad / stencil counts of
 // each voxel row.  All three run in one z-marching kernel:
 //
-//   CTA   = TJ voxel rows (j0..j0+TJ-1) x up to 1024 x-positions, marching
+//   CTA   = TJ voxel rows (j0..j0+TJ-1) x up to 256*E x-positions, marching
 //           over a z-chunk of voxel layers [kbeg, kend).
 //   stage = the TJ+1 grid rows of one lattice slice, staged in shared memory
 //           by the TMA engine (cp.async.bulk, one bulk copy per row) in a
 //           4-deep ring completed on mbarriers, so HBM streams while the SMs
 //           classify the previous slices.
-//   lane  = a chunk of 4 consecutive x positions (packed words).
+//   lane  = a 16-byte CHUNK of E = 16/sizeof(label) consecutive x positions.
 //
-// Per layer each thread first runs the FAST test on its chunk for every row:
-// the chunk's four grid rows are x-constant (incl. the next element) and equal
-// to each other -> no intersected edge, no point (the GPU analogue of the
-// paper's computational trimming: "rapidly skip portions of rows,
-// entire rows, and even entire data slices").  The surviving (row, chunk)
-// pairs are COMPACTED into a per-warp queue and processed with full lanes by
-// the SWAR slow path, which builds the 12 edge planes (X/Y/Z), the six face
-// planes (c^f), the point plane (c^e != 0) and counts with popc.
+// FAST test per (row, chunk): the chunk's four grid rows are x-constant
+// (incl. the next element) and equal to each other -> no intersected edge, no
+// point (the GPU analogue of the paper's computational trimming, P:121-124:
+// "rapidly skip portions of rows, entire rows, and even entire data slices").
+// It costs a few XOR/OR per 32-bit word, and one ballot per row hands the
+// warp its non-uniform lanes.  Those (row, chunk) TASKS are COMPACTED into a
+// CTA queue and drained every two layers with full lanes by the SWAR slow
+// path, which builds the 12 edge planes (X/Y/Z), the six face planes (c^f,
+// P:118), the point plane (c^e != 0) and counts with popc.
 //
 // Outputs per voxel row r = j + (N-1)(k - kA): cntP/cntQ/cntS (halo layers
 // count points only), the point trim [xL, xR) (P:124's final trim in voxel
@@ -49,18 +50,21 @@ struct CountArgs {
     int tma;                   // rows are 16-byte aligned: stage with cp.async.bulk
 };
 
-template <typename T> constexpr int count_tj() { return sizeof(T) == 1 ? 16 : (sizeof(T) == 2 ? 8 : 4); }
+template <typename T> __host__ __device__ constexpr int count_tj() { return 4; }
+template <typename T> __host__ __device__ constexpr int count_xt() { return 256 * Pack<T>::E; }   // x positions per CTA
 
 template <typename T, int TJ, bool ANZ>
 __global__ void __launch_bounds__(256) k_count(CountArgs a) {
-    constexpr int NW = Pack<T>::NW, NS = kCountStages, EB = Pack<T>::EB, EPW = Pack<T>::EPW;
-    constexpr int XT = 1024;                       // x positions per CTA
+    constexpr int NW = Pack<T>::NW, NS = kCountStages, EB = Pack<T>::EB, EPW = Pack<T>::EPW, E = Pack<T>::E;
+    constexpr int XT = count_xt<T>();
     constexpr int XPAD = 16 / (int)sizeof(T);      // extra elements staged (next element + 16-B rounding)
+    constexpr uint32_t CB = 16;                    // bytes per chunk
+    constexpr int WPR = XT / 32;                   // pmask words per row per CTA
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ __align__(8) uint64_t bars[NS];
     __shared__ uint32_t sP[2][TJ], sQ[2][TJ], sS[2][TJ];
     __shared__ int sL[2][TJ], sR[2][TJ];
-    __shared__ uint32_t spm[2][TJ][32];
+    __shared__ uint32_t spm[2][TJ][WPR];
     __shared__ uint16_t squeue[2 * TJ * 256];   // CTA task queue of a 2-layer batch: (layer bit, row, chunk)
     __shared__ uint32_t sqn;
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
@@ -77,9 +81,10 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
     const int64_t x_t0 = xt * XT;
     const int64_t xlen = min((int64_t)(XT + XPAD), M - x_t0);   // staged elements per row
     const uint32_t copy_bytes = (uint32_t)(xlen * (int64_t)sizeof(T));
-    const int64_t RB = a.RB;
-    const int64_t stage_bytes = (TJ + 1) * RB;
-    const int64_t x0 = x_t0 + 4 * (int64_t)tid;   // this thread's chunk
+    const uint32_t RB = (uint32_t)a.RB;
+    const uint32_t SB = (TJ + 1) * RB;                           // bytes per stage
+    const uint32_t sbase = smem_u32(dsm);
+    const int x0 = (int)(x_t0 + E * tid);                        // this thread's chunk
     const bool chunk_has_voxel = x0 <= M - 2;
 
     LabelSet ls = a.ls;
@@ -91,40 +96,40 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
         const int s = t / TJ, r = t % TJ;
         sP[s][r] = 0; sQ[s][r] = 0; sS[s][r] = 0; sL[s][r] = 0x7fffffff; sR[s][r] = -1;
     }
-    for (int t = tid; t < 2 * TJ * 32; t += blockDim.x) (&spm[0][0][0])[t] = 0u;
-    for (int64_t t = tid; t < NS * stage_bytes / 16; t += blockDim.x)
-        reinterpret_cast<uint4 *>(dsm)[t] = make_uint4(0, 0, 0, 0);
+    for (int t = tid; t < 2 * TJ * WPR; t += blockDim.x) (&spm[0][0][0])[t] = 0u;
+    for (uint32_t t = tid; t < NS * SB / 16; t += blockDim.x) reinterpret_cast<uint4 *>(dsm)[t] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
+        sqn = 0;
     }
     __syncthreads();
     if (kbeg >= kend) return;
     const int64_t nsteps = kend - kbeg;           // voxel layers; slices kbeg..kend
 
     const T *lab = reinterpret_cast<const T *>(a.labels);
-    auto row_src = [&](int64_t s, int g) -> const T * {
-        const int64_t j = min(j0 + g, N - 1);
-        return lab + ((s - a.z_lo) * N + j) * M + x_t0;
-    };
-    // Fill the stage of slice ordinal o (slice kbeg + o).  TMA: one elected
-    // thread; fallback (rows not 16-B aligned): all threads copy.
+    // Fill the stage of slice ordinal o (slice kbeg + o).  TMA: lanes 0..TJ of
+    // warp 0 issue one bulk copy per row; fallback (rows not 16-B aligned):
+    // all threads copy.  Must be called by the whole CTA.
     auto fill = [&](int64_t o) {
         const int st = (int)(o % NS);
-        uint8_t *base = dsm + st * stage_bytes;
         if (a.tma) {
-            if (tid == 0) {
-                fence_proxy_async();   // prior generic reads of this stage precede the async-proxy writes
-                mbar_expect_tx(&bars[st], copy_bytes * (TJ + 1));
-#pragma unroll 1
-                for (int g = 0; g <= TJ; ++g)
-                    tma_load_1d(base + g * RB, row_src(kbeg + o, g), copy_bytes, &bars[st]);
+            if (warp == 0) {
+                if (lane == 0) mbar_expect_tx(&bars[st], copy_bytes * (TJ + 1));
+                __syncwarp();
+                if (lane <= TJ) {
+                    fence_proxy_async();   // prior generic reads of this stage precede the async-proxy writes
+                    const int64_t j = min(j0 + lane, N - 1);
+                    const T *src = lab + ((kbeg + o - a.z_lo) * N + j) * M + x_t0;
+                    tma_load_1d(dsm + st * SB + lane * RB, src, copy_bytes, &bars[st]);
+                }
             }
         } else {
             for (int64_t t = tid; t < (TJ + 1) * xlen; t += blockDim.x) {
                 const int g = (int)(t / xlen);
                 const int64_t x = t % xlen;
-                reinterpret_cast<T *>(base + g * RB)[x] = row_src(kbeg + o, g)[x];
+                const int64_t j = min(j0 + g, N - 1);
+                reinterpret_cast<T *>(dsm + st * SB + g * RB)[x] = lab[((kbeg + o - a.z_lo) * N + j) * M + x_t0 + x];
             }
         }
     };
@@ -134,58 +139,35 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
     for (int64_t o = 0; o < NS && o <= nsteps; ++o) fill(o);
     if (!a.tma) __syncthreads();
 
-    auto chunk_at = [&](int64_t o, int g, int64_t c, uint32_t (&w)[NW], uint32_t &nxt) {
-        const uint8_t *p = dsm + (o % NS) * stage_bytes + g * RB + 4 * c * (int64_t)sizeof(T);
-        if constexpr (NW == 1) { w[0] = *reinterpret_cast<const uint32_t *>(p); }
-        else if constexpr (NW == 2) { uint2 v = *reinterpret_cast<const uint2 *>(p); w[0] = v.x; w[1] = v.y; }
-        else { uint4 v = *reinterpret_cast<const uint4 *>(p); w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
-        nxt = *reinterpret_cast<const uint32_t *>(p + 4 * sizeof(T));
+    // shared address of chunk c of row g of the stage holding slice ordinal o
+    auto saddr = [&](int64_t o, int g, int c) -> uint32_t {
+        return sbase + (uint32_t)(o % NS) * SB + (uint32_t)g * RB + (uint32_t)c * CB;
+    };
+    auto chunk_at = [&](uint32_t addr, uint32_t (&w)[NW], uint32_t &nxt) {
+        lds_chunk<T>(addr, w);
+        nxt = lds32(addr + CB);
         if (!ANZ) { remap<T>(ls, w); nxt = remap1<T>(ls, nxt); }
     };
 
-    // Per-slice flags of this thread's chunk: huM bit g = row g x-constant
-    // (incl. the next element); eqYM bit g = rows g and g+1 equal.
-    uint32_t Wa[TJ + 1][NW], Wb[TJ + 1][NW];
-    uint32_t huA = 0, eqA = 0, huB = 0, eqB = 0;
-    auto load_flags = [&](int64_t o, uint32_t (&W)[TJ + 1][NW], uint32_t &hu, uint32_t &eqy) {
-        hu = 0; eqy = 0;
-#pragma unroll
-        for (int g = 0; g <= TJ; ++g) {
-            uint32_t nxt, h[NW];
-            chunk_at(o, g, tid, W[g], nxt);
-            shift1<T>(W[g], nxt, h);
-            bool e = true;
-#pragma unroll
-            for (int q = 0; q < NW; ++q) e = e && (W[g][q] == h[q]);
-            hu |= (e ? 1u : 0u) << g;
-        }
-#pragma unroll
-        for (int g = 0; g < TJ; ++g) {
-            bool e = true;
-#pragma unroll
-            for (int q = 0; q < NW; ++q) e = e && (W[g][q] == W[g + 1][q]);
-            eqy |= (e ? 1u : 0u) << g;
-        }
-    };
-
-    const int64_t nrows = N - 1 - j0;   // voxel rows of this block (may be < TJ at the edge)
-    const uint32_t rows_valid = (nrows >= TJ) ? ((1u << TJ) - 1u) : ((1u << (uint32_t)(nrows > 0 ? nrows : 0)) - 1u);
+    const int nrows = (int)(N - 1 - j0);   // voxel rows of this block (may be < TJ at the edge)
+    const uint32_t rows_valid = (nrows >= TJ) ? ((1u << TJ) - 1u) : ((1u << (nrows > 0 ? nrows : 0)) - 1u);
 
     // Slow path for one (row r, chunk c) task of voxel layer k (slices o, o+1).
     auto process_task = [&](int64_t o, int r, int c, int64_t k, bool own, int slot) {
         uint32_t A[NW], B[NW], C[NW], D[NW], hA[NW], hB[NW], hC[NW], hD[NW], n;
-        chunk_at(o, r, c, A, n); shift1<T>(A, n, hA);
-        chunk_at(o, r + 1, c, B, n); shift1<T>(B, n, hB);
-        chunk_at(o + 1, r, c, C, n); shift1<T>(C, n, hC);
-        chunk_at(o + 1, r + 1, c, D, n); shift1<T>(D, n, hD);
-        const int64_t xc = x_t0 + 4 * (int64_t)c, j = j0 + r;
+        chunk_at(saddr(o, r, c), A, n); shift1<T>(A, n, hA);
+        chunk_at(saddr(o, r + 1, c), B, n); shift1<T>(B, n, hB);
+        chunk_at(saddr(o + 1, r, c), C, n); shift1<T>(C, n, hC);
+        chunk_at(saddr(o + 1, r + 1, c), D, n); shift1<T>(D, n, hD);
+        const int xc = (int)x_t0 + E * c;
+        const int64_t j = j0 + r;
         uint32_t mvox[NW], mi1[NW], miM3[NW];
 #pragma unroll
         for (int q = 0; q < NW; ++q) { mvox[q] = 0; mi1[q] = 0; miM3[q] = 0; }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < E; ++e) {
             const uint32_t bit = 1u << ((EB * (e % EPW) + EB - 1) & 31);
-            const int64_t i = xc + e;
+            const int i = xc + e;
             if (i <= M - 2) mvox[e / EPW] |= bit;
             if (i >= 1) mi1[e / EPW] |= bit;
             if (i <= M - 3) miM3[e / EPW] |= bit;
@@ -218,58 +200,80 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
                 if (k <= a.O - 3) cs += __popc(Fpz & mvox[q]);
             }
         }
-        uint32_t nib = 0;
+        uint32_t bits = 0;   // point bits of the chunk's E voxels
 #pragma unroll
-        for (int e = 0; e < 4; ++e) nib |= flag<T>(pt, e) << e;
-        if (nib) {
-            atomicAdd(&sP[slot][r], (uint32_t)__popc(nib));
+        for (int e = 0; e < E; ++e) bits |= flag<T>(pt, e) << e;
+        if (bits) {
+            const int wofs = (E * c) & 31;   // E divides 32: the chunk lies inside one pmask word
+            atomicAdd(&sP[slot][r], (uint32_t)__popc(bits));
             atomicAdd(&sQ[slot][r], cq);
             atomicAdd(&sS[slot][r], cs);
-            atomicOr(&spm[slot][r][c >> 3], nib << (4 * (c & 7)));
-            atomicMin(&sL[slot][r], (int)(xc + __ffs(nib) - 1));
-            atomicMax(&sR[slot][r], (int)(xc + 31 - __clz(nib)));
+            atomicOr(&spm[slot][r][(E * c) >> 5], bits << wofs);
+            atomicMin(&sL[slot][r], xc + __ffs(bits) - 1);
+            atomicMax(&sR[slot][r], xc + 31 - __clz(bits));
         }
     };
 
-    // FAST test of one layer: every thread checks its chunk for the TJ rows and
-    // appends the non-uniform (row, chunk) pairs to the CTA queue.
-    auto fast = [&](int64_t o, const uint32_t (&Wl)[TJ + 1][NW], uint32_t hul, uint32_t eql,
-                    const uint32_t (&Wh)[TJ + 1][NW], uint32_t huh, uint32_t eqh) {
-        uint32_t eqz = 0;
+    // Per-slice row flags of this thread's chunk: rf[r] != 0 iff grid rows r and
+    // r+1 of the slice are not both x-constant (incl. the next element) and
+    // equal to each other.  slice_flags() computes the new slice's flags and,
+    // against the previous slice's, appends the slow (row, chunk) tasks of
+    // voxel layer o-1 to the CTA queue: one ballot per row gives the warp the
+    // row's task lanes, one atomic per warp reserves the queue slots.
+    uint32_t rfA[TJ], rfB[TJ];
+    const uint32_t lt = (1u << lane) - 1u;
+    auto slice_flags = [&](int64_t o, uint32_t (&rf)[TJ], const uint32_t (&rfl)[TJ], bool with_lo) {
+        uint32_t Wp[NW], xdp = 0, b[TJ];
+        uint32_t addr = saddr(o, 0, tid), addr_lo = saddr(o - 1, 0, tid);
+#pragma unroll
+        for (int g = 0; g <= TJ; ++g) {
+            uint32_t W[NW], H[NW], nn;
+            chunk_at(addr, W, nn);
+            shift1<T>(W, nn, H);
+            uint32_t xd = 0;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) xd |= W[q] ^ H[q];
+            if (g > 0) {
+                uint32_t yd = 0;
+#pragma unroll
+                for (int q = 0; q < NW; ++q) yd |= Wp[q] ^ W[q];
+                rf[g - 1] = xdp | xd | yd;
+                if (with_lo) {
+                    uint32_t Wo[NW];
+                    lds_chunk<T>(addr_lo, Wo);
+                    addr_lo += RB;
+                    if (!ANZ) remap<T>(ls, Wo);
+                    uint32_t zd = 0;
+#pragma unroll
+                    for (int q = 0; q < NW; ++q) zd |= Wo[q] ^ Wp[q];
+                    const bool row_ok = ((rows_valid >> (g - 1)) & 1u) && chunk_has_voxel;
+                    b[g - 1] = __ballot_sync(kFull, row_ok && (rfl[g - 1] | rf[g - 1] | zd) != 0u);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NW; ++q) Wp[q] = W[q];
+            xdp = xd;
+            addr += RB;
+        }
+        if (!with_lo) return;
+        uint32_t total = 0;
+#pragma unroll
+        for (int r = 0; r < TJ; ++r) total += __popc(b[r]);
+        if (total == 0) return;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&sqn, total);
+        base = __shfl_sync(kFull, base, 0);
+        const uint32_t tag = (uint32_t)((o - 1) & 1) << 15 | (uint32_t)tid;
 #pragma unroll
         for (int r = 0; r < TJ; ++r) {
-            bool e = true;
-#pragma unroll
-            for (int q = 0; q < NW; ++q) e = e && (Wl[r][q] == Wh[r][q]);
-            eqz |= (e ? 1u : 0u) << r;
-        }
-        const uint32_t uni = hul & (hul >> 1) & huh & (huh >> 1) & eql & eqh & eqz;
-        const uint32_t slow = chunk_has_voxel ? (~uni & rows_valid) : 0u;
-        const uint32_t cnt = __popc(slow);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, incl, d);
-            if (lane >= d) incl += y;
-        }
-        const uint32_t total = __shfl_sync(kFull, incl, 31);
-        if (total) {
-            uint32_t pos = 0;
-            if (lane == 31) pos = atomicAdd(&sqn, total);
-            pos = __shfl_sync(kFull, pos, 31) + incl - cnt;
-            uint32_t m = slow;
-            const uint32_t tag = (uint32_t)(o & 1) << 15 | (uint32_t)tid;
-            while (m) {
-                const int r = __ffs(m) - 1;
-                m &= m - 1;
-                squeue[pos++] = (uint16_t)(tag | (uint32_t)r << 8);
-            }
+            if ((b[r] >> lane) & 1u) squeue[base + __popc(b[r] & lt)] = (uint16_t)(tag | (uint32_t)r << 8);
+            base += __popc(b[r]);
         }
     };
 
     // SLOW phase of a batch of 1-2 layers [o0, o0+nb): all threads drain the
     // CTA queue with full lanes, then the layers' rows are flushed and their
-    // lower slices released to the TMA producer.
+    // lower slices released to the TMA engine.
     auto batch = [&](int64_t o0, int nb) {
         __syncthreads();
         const uint32_t nq = sqn;
@@ -287,19 +291,20 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
             const int64_t o = o0 + b;
             const int64_t k = kbeg + o;
             const int slot = (int)(o & 1);
-            for (int t = tid; t < TJ * 32; t += blockDim.x) {
-                const int r = t >> 5, w = t & 31;
-                const int64_t gw = (x_t0 >> 5) + w;
-                if (((rows_valid >> r) & 1u) && gw < a.W32) {
-                    const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
-                    a.pmask[rr * a.W32 + gw] = spm[slot][r][w];
-                }
+            const int64_t row0 = j0 + (N - 1) * (k - a.kA);
+            uint32_t *pm0 = a.pmask + row0 * a.W32 + (x_t0 >> 5);
+            const uint32_t W32 = (uint32_t)a.W32;
+            const int64_t wrem = a.W32 - (x_t0 >> 5);
+            const uint32_t wlim = wrem < WPR ? (uint32_t)wrem : (uint32_t)WPR;
+            for (int t = tid; t < TJ * WPR; t += blockDim.x) {
+                const uint32_t r = (uint32_t)t / WPR, w = (uint32_t)t % WPR;
+                if (((rows_valid >> r) & 1u) && w < wlim) pm0[r * W32 + w] = spm[slot][r][w];
                 spm[slot][r][w] = 0u;
             }
             if (tid < TJ) {
                 const int r = tid;
                 if ((rows_valid >> r) & 1u) {
-                    const int64_t rr = j0 + r + (N - 1) * (k - a.kA);
+                    const int64_t rr = row0 + r;
                     const uint32_t p = sP[slot][r];
                     const int xl = p ? sL[slot][r] : 0, xr = p ? sR[slot][r] + 1 : 0;
                     if (!a.multi_xt) {
@@ -318,19 +323,15 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
         }
     };
 
-    if (tid == 0) sqn = 0;
-    __syncthreads();
     wait(0);
-    load_flags(0, Wa, huA, eqA);
+    slice_flags(0, rfA, rfB, false);
     for (int64_t o = 0; o < nsteps; o += 2) {
         wait(o + 1);
-        load_flags(o + 1, Wb, huB, eqB);
-        fast(o, Wa, huA, eqA, Wb, huB, eqB);
+        slice_flags(o + 1, rfB, rfA, true);
         const bool two = o + 1 < nsteps;
         if (two) {
             wait(o + 2);
-            load_flags(o + 2, Wa, huA, eqA);
-            fast(o + 1, Wb, huB, eqB, Wa, huA, eqA);
+            slice_flags(o + 2, rfA, rfB, true);
         }
         batch(o, two ? 2 : 1);
     }

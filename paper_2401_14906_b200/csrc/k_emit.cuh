@@ -92,8 +92,13 @@ __global__ void __launch_bounds__(256, 3) k_emit(EmitArgs a) {
     const T *lab = reinterpret_cast<const T *>(a.labels);
 
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t rr = blockIdx.x * (blockDim.x >> 5) + warp; rr < R; rr += warps) {
-        if (__ldg(a.cntP + rr) == 0) continue;
+    uint32_t rr = blockIdx.x * (blockDim.x >> 5) + warp;
+    uint32_t cnt_next = rr < R ? __ldg(a.cntP + rr) : 0u;
+    for (; rr < R; rr += warps) {
+        // software pipelining: the next row's point count is in flight while this row is emitted
+        const uint32_t cnt = cnt_next;
+        cnt_next = (rr + warps < R) ? __ldg(a.cntP + rr + warps) : 0u;
+        if (cnt == 0) continue;
         const uint32_t j = rr % NV, k = kA + rr / NV;
         const bool own = (k >= own0) && (k < own1);
         // neighbour rows (j-1,k-1), (j,k-1), (j-1,k), (j+1,k), (j,k+1); -1 = absent

@@ -270,21 +270,25 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
 
     if (phase & PSN_COUNT) {
         if (cudaMemsetAsync(at<char>(ws, L.hdr), 0, L.cntP - L.hdr, st) != cudaSuccess) return cuda_check(ctx, "memset");
-        const int64_t chunks = (L.M - 1 + 3) / 4;            // 4-voxel lane chunks per row
-        const int64_t nXT = (chunks + 255) / 256;             // 1024 x-positions per CTA
+        const int64_t E = 16 / eb;                            // elements per 16-byte lane chunk
+        const int64_t chunks = (L.M - 1 + E - 1) / E;        // lane chunks per row
+        const int64_t nXT = (chunks + 255) / 256;             // 256 chunks (256*E x-positions) per CTA
         const int64_t WX = std::min<int64_t>((chunks + 31) / 32, 8);
         const int tj = eb == 1 ? count_tj<uint8_t>() : (eb == 2 ? count_tj<uint16_t>() : count_tj<uint32_t>());
         const int64_t nJB = (L.N - 1 + tj - 1) / tj;
         const int64_t nLay = L.kB - L.kA;
-        const int64_t target_warps = (int64_t)ctx->sms * 32;
-        int64_t nZC = std::max<int64_t>(1, (target_warps + nXT * nJB * WX - 1) / (nXT * nJB * WX));
+        // z-chunks: ~8 waves of CTAs (4 resident per SM) so the last wave's tail is small,
+        // while each CTA still marches >= 16 layers to amortise its TMA prologue
+        const int64_t target_ctas = (int64_t)ctx->sms * 4 * 8;
+        int64_t nZC = std::max<int64_t>(1, (target_ctas + nXT * nJB - 1) / (nXT * nJB));
+        nZC = std::min(nZC, std::max<int64_t>(1, nLay / 16));
         nZC = std::min(nZC, nLay);
         const int64_t KZ = (nLay + nZC - 1) / nZC;
         nZC = (nLay + KZ - 1) / KZ;
         const int64_t xpad = 16 / eb;
-        // every thread of the CTA reads its 4-element chunk and the next word, so a staged row
+        // every thread of the CTA reads its 16-byte chunk and the next word, so a staged row
         // spans the CTA's full width (zero-filled past the row end), plus the 16-byte pad
-        const int64_t RB = (int64_t)align16((size_t)((128 * WX + xpad) * eb));
+        const int64_t RB = (int64_t)align16((size_t)((32 * WX * E + xpad) * eb));
         const size_t smem = (size_t)kCountStages * (size_t)(tj + 1) * (size_t)RB;
         CountArgs ca;
         ca.labels = slab0; ca.M = L.M; ca.N = L.N; ca.O = L.O; ca.z_lo = vol->z_lo;

@@ -21,17 +21,19 @@ namespace psn {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kBackground = 0xFFFFFFFFu;
 
+// A lane's CHUNK is 16 bytes of a grid row: E = 16/sizeof(T) consecutive
+// elements in NW = 4 packed 32-bit words (EPW elements per word, EB bits each).
 template <typename T> struct Pack;
 template <> struct Pack<uint8_t> {
-    static constexpr int NW = 1, EB = 8, EPW = 4;
+    static constexpr int NW = 4, EB = 8, EPW = 4, E = 16;
     static constexpr uint32_t LOW = 0x7F7F7F7Fu, MSB = 0x80808080u, EMASK = 0xFFu;
 };
 template <> struct Pack<uint16_t> {
-    static constexpr int NW = 2, EB = 16, EPW = 2;
+    static constexpr int NW = 4, EB = 16, EPW = 2, E = 8;
     static constexpr uint32_t LOW = 0x7FFF7FFFu, MSB = 0x80008000u, EMASK = 0xFFFFu;
 };
 template <> struct Pack<uint32_t> {
-    static constexpr int NW = 4, EB = 32, EPW = 1;
+    static constexpr int NW = 4, EB = 32, EPW = 1, E = 4;
     static constexpr uint32_t LOW = 0x7FFFFFFFu, MSB = 0x80000000u, EMASK = 0xFFFFFFFFu;
 };
 
@@ -57,63 +59,18 @@ __device__ __forceinline__ void shift1(const uint32_t (&w)[Pack<T>::NW], uint32_
     }
 }
 
-// Flag bit of element e (0..3) of a spread plane.
+// Flag bit of element e (0..E-1) of a spread plane.
 template <typename T>
 __device__ __forceinline__ uint32_t flag(const uint32_t (&p)[Pack<T>::NW], int e) {
     constexpr int EPW = Pack<T>::EPW, EB = Pack<T>::EB;
     return (p[e / EPW] >> (EB * (e % EPW) + EB - 1)) & 1u;
 }
 
-// Raw element e (0..3) of a packed chunk.
+// Raw element e (0..E-1) of a packed chunk.
 template <typename T>
 __device__ __forceinline__ uint32_t elem(const uint32_t (&w)[Pack<T>::NW], int e) {
     constexpr int EPW = Pack<T>::EPW, EB = Pack<T>::EB;
     return (EB == 32) ? w[e] : ((w[e / EPW] >> (EB * (e % EPW))) & Pack<T>::EMASK);
-}
-
-// ---------------------------------------------------------------- loaders
-// Chunk of 4 elements starting at x0 (multiple of 4) of a row of M elements.
-// VEC: one aligned vector load when the chunk is complete (requires rows
-// aligned to 4*NW bytes, i.e. M % 4 == 0 and a 16-byte aligned base).
-// Elements >= M are zero-filled (they belong to no voxel).
-template <typename T, bool VEC>
-__device__ __forceinline__ void load_chunk(const T *__restrict__ row, int64_t x0, int64_t M,
-                                           uint32_t (&w)[Pack<T>::NW]) {
-    constexpr int NW = Pack<T>::NW;
-    if (VEC && x0 + 4 <= M) {
-        if constexpr (NW == 1) {
-            w[0] = __ldg(reinterpret_cast<const uint32_t *>(row + x0));
-        } else if constexpr (NW == 2) {
-            uint2 v = __ldg(reinterpret_cast<const uint2 *>(row + x0));
-            w[0] = v.x; w[1] = v.y;
-        } else {
-            uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + x0));
-            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-        }
-        return;
-    }
-#pragma unroll
-    for (int q = 0; q < NW; ++q) w[q] = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        uint32_t v = (x0 + e < M) ? (uint32_t)__ldg(row + x0 + e) : 0u;
-        w[e / Pack<T>::EPW] |= v << (Pack<T>::EB * (e % Pack<T>::EPW) % 32);
-    }
-}
-
-// First packed word of the chunk starting at x0 (used for the element after a
-// lane's chunk when it lives in another warp).
-template <typename T, bool VEC>
-__device__ __forceinline__ uint32_t load_word(const T *__restrict__ row, int64_t x0, int64_t M) {
-    constexpr int EPW = Pack<T>::EPW;
-    if (VEC && x0 + EPW <= M) return __ldg(reinterpret_cast<const uint32_t *>(row + x0));
-    uint32_t w = 0;
-#pragma unroll
-    for (int e = 0; e < EPW; ++e) {
-        uint32_t v = (x0 + e < M) ? (uint32_t)__ldg(row + x0 + e) : 0u;
-        w |= v << (Pack<T>::EB * e % 32);
-    }
-    return w;
 }
 
 // ---------------------------------------------------------------- classification
@@ -235,5 +192,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+}  // namespace psn
+
+// ---------------------------------------------------------------- 32-bit shared-memory loads
+namespace psn {
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+// The 4-element chunk (NW packed words) at shared address addr.
+template <typename T>
+__device__ __forceinline__ void lds_chunk(uint32_t addr, uint32_t (&w)[Pack<T>::NW]) {
+    if constexpr (Pack<T>::NW == 1) { w[0] = lds32(addr); }
+    else if constexpr (Pack<T>::NW == 2) { const uint2 v = lds64(addr); w[0] = v.x; w[1] = v.y; }
+    else { const uint4 v = lds128(addr); w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
 }
 }  // namespace psn
