@@ -81,7 +81,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -366,7 +366,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-voxels", type=float, default=24e6, help="oracle sample size for cpu_baseline")
+    ap.add_argument("--cpu-voxels", type=float, default=96e6, help="oracle sample size for cpu_baseline (~10-30 s)")
     ap.add_argument("--ref-voxels", type=float, default=6e6, help="oracle sample size per reference step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
