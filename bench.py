@@ -91,7 +91,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, start: bool):
+        """Bracket the timed region (samples outside it are dropped, nearest kept if none)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def __exit__(self, *exc):
         if self.proc:
@@ -105,7 +112,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons, util = [], [], set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", 1e300)
+        inside = [ln for ts, ln in self.lines if t0 <= ts <= t1 + 0.05]
+        if not inside and self.lines:   # region shorter than the sampling period: nearest samples
+            inside = [ln for ts, ln in sorted(self.lines, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))[:2]]
+        for ln in inside:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -245,6 +256,7 @@ def run_psn(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    clk = ClockSampler(local_rank)
     # warm-up (W >= 3)
     for _ in range(args.warmup):
         run_extract()
@@ -260,17 +272,22 @@ def run_psn(args, rank, world, local_rank):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        for s in range(K):
-            ev[s][0].record(stream)
-            run_extract()
-            ev[s][1].record(stream)
-            run_smooth()
-            ev[s][2].record(stream)
-        torch.cuda.synchronize()
-        barrier()
+    clk.__enter__()
+    time.sleep(0.5)          # nvidia-smi needs a moment before its first sample
+    barrier()
+    torch.cuda.synchronize()
+    clk.mark(True)
+    for s in range(K):
+        ev[s][0].record(stream)
+        run_extract()
+        ev[s][1].record(stream)
+        run_smooth()
+        ev[s][2].record(stream)
+    torch.cuda.synchronize()
+    clk.mark(False)
+    barrier()
+    time.sleep(0.05)
+    clk.__exit__(None, None, None)
     t_ext = sum(e[0].elapsed_time(e[1]) for e in ev) / K    # ms per step
     t_sm = sum(e[1].elapsed_time(e[2]) for e in ev) / K
     t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / K

@@ -25,8 +25,10 @@
 //
 // Outputs per voxel row r = j + (N-1)(k - kA): cntP/cntQ/cntS (halo layers
 // count points only), the point trim [xL, xR) (P:124's final trim in voxel
-// units; [0,0) when empty) and the point bit-plane pmask[r][w] in natural
-// order (bit b of word w <-> voxel 32w + b).
+// units; [0,0) when empty), the point bit-plane pmask[r][w] in natural
+// order (bit b of word w <-> voxel 32w + b) and ppre[r][w], the number of
+// points of row r before word w inside the CTA's x-tile (the row iterator's
+// running id, precomputed per word so Pass 4 needs no row scans).
 #pragma once
 #include "psn_common.cuh"
 
@@ -45,6 +47,7 @@ struct CountArgs {
     uint32_t *cntP, *cntQ, *cntS;
     int2 *trim;
     uint32_t *pmask;
+    uint16_t *ppre;            // per pmask word: points before it within the CTA's x-tile
     LabelSet ls;
     int multi_xt;              // several x-tiles per row: accumulate with global atomics
     int tma;                   // rows are 16-byte aligned: stage with cp.async.bulk
@@ -293,13 +296,31 @@ __global__ void __launch_bounds__(256) k_count(CountArgs a) {
             const int slot = (int)(o & 1);
             const int64_t row0 = j0 + (N - 1) * (k - a.kA);
             uint32_t *pm0 = a.pmask + row0 * a.W32 + (x_t0 >> 5);
+            uint16_t *pp0 = a.ppre + row0 * a.W32 + (x_t0 >> 5);
             const uint32_t W32 = (uint32_t)a.W32;
             const int64_t wrem = a.W32 - (x_t0 >> 5);
             const uint32_t wlim = wrem < WPR ? (uint32_t)wrem : (uint32_t)WPR;
-            for (int t = tid; t < TJ * WPR; t += blockDim.x) {
-                const uint32_t r = (uint32_t)t / WPR, w = (uint32_t)t % WPR;
-                if (((rows_valid >> r) & 1u) && w < wlim) pm0[r * W32 + w] = spm[slot][r][w];
-                spm[slot][r][w] = 0u;
+            // point planes + per-word point prefix within this x-tile (one warp per row)
+            constexpr int PPL = WPR / 32;   // words per lane
+            for (int r = warp; r < TJ; r += (int)(blockDim.x >> 5)) {
+                uint32_t wv[PPL], cnt = 0;
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) { wv[q] = spm[slot][r][lane * PPL + q]; cnt += __popc(wv[q]); }
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                uint32_t pre = incl - cnt;
+                const bool rv = (rows_valid >> r) & 1u;
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) {
+                    const uint32_t w = (uint32_t)(lane * PPL + q);
+                    if (rv && w < wlim) { pm0[r * W32 + w] = wv[q]; pp0[r * W32 + w] = (uint16_t)pre; }
+                    pre += __popc(wv[q]);
+                    spm[slot][r][w] = 0u;
+                }
             }
             if (tid < TJ) {
                 const int r = tid;

@@ -62,7 +62,7 @@ size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 
 struct Layout {
     int64_t M, N, O, kA, kB, R, W32, nTiles;
-    size_t hdr, tiles, cntP, cntQ, cntS, offP, offQ, offS, trim, pmask, labels, total;
+    size_t hdr, tiles, cntP, cntQ, cntS, offP, offQ, offS, trim, pmask, ppre, labels, total;
 };
 
 constexpr int64_t kMaxList = 65536;   // u32 label-subset capacity in the workspace
@@ -99,6 +99,7 @@ psn_status layout(psn_ctx *ctx, const psn_volume *v, Layout *L) {
     L->offS = off; off += align_up(4 * (size_t)L->R);
     L->trim = off; off += align_up(8 * (size_t)L->R);
     L->pmask = off; off += align_up(4 * (size_t)L->R * (size_t)L->W32);
+    L->ppre = off; off += align_up(2 * (size_t)L->R * (size_t)L->W32);
     L->labels = off;
     off += align_up(v->dtype == PSN_U32 ? 4 * (size_t)kMaxList : 8192);
     L->total = off;
@@ -170,9 +171,14 @@ cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int th
 }
 
 template <typename T>
-void dispatch_emit(const EmitArgs &ea, bool anz, int64_t blocks, cudaStream_t st) {
-    if (anz) k_emit<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
-    else k_emit<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
+void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st) {
+    if (fast) {   // rows fit one k_count x-tile: per-word point prefixes are row prefixes
+        if (anz) k_emit_fast<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
+        else k_emit_fast<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
+    } else {
+        if (anz) k_emit<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
+        else k_emit<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
+    }
 }
 
 std::array<int64_t, 6> signature(const psn_volume *v) {
@@ -295,7 +301,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W32 = L.W32;
         ca.nXT = nXT; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB;
         ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
-        ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask);
+        ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask); ca.ppre = at<uint16_t>(ws, L.ppre);
         ca.ls = ls; ca.multi_xt = nXT > 1 ? 1 : 0;
         ca.tma = ((L.M * eb) % 16 == 0) && ((reinterpret_cast<uintptr_t>(slab0) & 15u) == 0);
         const int64_t gridR = std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8);
@@ -347,6 +353,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.kA = L.kA; ea.kB = L.kB; ea.own_k0 = vol->own_k0; ea.own_k1 = vol->own_k1; ea.W32 = L.W32; ea.R = L.R;
     ea.cntP = at<uint32_t>(ws, L.cntP); ea.offP = at<uint32_t>(ws, L.offP);
     ea.offQ = at<uint32_t>(ws, L.offQ); ea.offS = at<uint32_t>(ws, L.offS); ea.pmask = at<uint32_t>(ws, L.pmask);
+    ea.ppre = at<uint16_t>(ws, L.ppre);
     ea.ls = ls;
     for (int a = 0; a < 3; ++a) { ea.sp[a] = vol->spacing[a]; ea.org[a] = vol->origin[a]; }
     ea.points = mesh->points; ea.quads = mesh->quads; ea.pairs = mesh->pairs;
@@ -356,9 +363,10 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.first_stencil = (uint32_t)mesh->first_stencil;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
-    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, blocks, st);
-    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, blocks, st);
-    else dispatch_emit<uint32_t>(ea, anz, blocks, st);
+    const bool fast = (L.M - 1) <= (int64_t)(eb == 1 ? count_xt<uint8_t>() : eb == 2 ? count_xt<uint16_t>() : count_xt<uint32_t>());
+    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, fast, blocks, st);
+    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st);
+    else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st);
     ++ctx->launches;
     return cuda_check(ctx, "emit launch");
 }
