@@ -265,7 +265,7 @@ int oracle_extract(const void *labels, int elem_bytes,
 
     int64_t nP = 0, nQ = 0, nS = 0;
     int over = 0;
-    if (csr_off && capP >= 1) csr_off[0] = (uint32_t)stencil_base;
+    if (csr_off) csr_off[0] = (uint32_t)stencil_base;   /* caller allocates capP + 1 entries */
     for (int64_t k = k0; k < k1; ++k)
         for (int64_t j = 0; j < VY; ++j)
             for (int64_t i = 0; i < VX; ++i) {
