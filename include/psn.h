@@ -153,8 +153,8 @@ psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh,
 /* Workspace of the smoothing calls: the smoothing cache (the
  * extracted mesh is kept so re-smoothing skips re-extraction) -- a fixed-stride
  * uint32[P][4] table of each own point's -z,-y,+y,+z neighbour window indices
- * -- followed by two fp32 [n_window][3] index-space offset buffers (used by
- * psn_smooth's double buffering). */
+ * -- followed by two [n_window] index-space offset buffers (double buffering,
+ * P:94) and the wavefront schedule (tile ranges, per-tile progress). */
 psn_status psn_smooth_workspace(const psn_mesh *mesh, size_t *bytes);
 
 /* Build the smoothing cache of `mesh` into ws (psn_smooth does this itself;
@@ -186,6 +186,20 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
  */
 psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, const float *src,
                            float *dst, float relaxation, float constraint_distance, void *stream);
+
+/* Smoothing strategy of psn_smooth (whole volume):
+ *   PSN_SMOOTH_PER_ITERATION (default): one launch per Jacobi iteration.
+ *   PSN_SMOOTH_WAVEFRONT: G iterations per persistent launch, scheduled as a
+ *     wavefront over tiles of consecutive points so each tile's state stays
+ *     L2-resident across iterations (iterations_per_launch G, 0 = chosen
+ *     from the L2 size; points_per_tile a multiple of 256, 0 = 1024).
+ *     Bit-identical to the default; measured slower on B200. */
+enum { PSN_SMOOTH_WAVEFRONT = 0, PSN_SMOOTH_PER_ITERATION = 1 };
+psn_status psn_ctx_set_smoothing(psn_ctx *ctx, int mode, int32_t iterations_per_launch, int32_t points_per_tile);
+
+/* Synchronising check of the last psn_smooth on ws: PSN_ERR_CUDA if a
+ * wavefront dependency wait timed out (a guard that must never trigger). */
+psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, void *stream);
 
 /* World coordinates of window entries [w0, w1) from offsets (NULL = anchors). */
 psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,

@@ -38,6 +38,41 @@ __device__ __forceinline__ float world_of(float p, float o, double org, double s
     return __double2float_rn(__dadd_rn(anchor64_from(p, org, sp), __dmul_rn(sp, (double)o)));
 }
 
+// One Jacobi update of Eq. 1 on index-space offsets (shared by k_smooth and
+// k_smooth_tb, so both strategies are bit-identical).  f = face mask (bits
+// -z,-y,-x,+x,+y,+z), o = own offset, mx/px = -x/+x neighbours, g0..g3 =
+// -z,-y,+y,+z neighbours (values of absent faces are ignored).
+//   s = e + sum_j o_j - deg * o          (e = sum of the face directions)
+//   o' = clamp(o + lambda * s * (1/deg), -d, d)      (readings Q8, Q9, Q10)
+// Explicit _rn intrinsics: no FMA contraction, a fixed summation order.
+__device__ __forceinline__ float jacobi_axis(float e, float o, float mx, float px, float g0, float g1, float g2,
+                                             float g3, uint32_t f, float fd, float inv, float lambda, float d) {
+    float acc = 0.f;
+    if (f & 4u) acc = __fadd_rn(acc, mx);
+    if (f & 8u) acc = __fadd_rn(acc, px);
+    if (f & 1u) acc = __fadd_rn(acc, g0);
+    if (f & 2u) acc = __fadd_rn(acc, g1);
+    if (f & 16u) acc = __fadd_rn(acc, g2);
+    if (f & 32u) acc = __fadd_rn(acc, g3);
+    const float sum = __fadd_rn(__fadd_rn(e, acc), -__fmul_rn(fd, o));
+    return fminf(fmaxf(__fadd_rn(o, __fmul_rn(lambda, __fmul_rn(sum, inv))), -d), d);
+}
+
+__device__ __forceinline__ float3 jacobi_update(uint32_t f, float3 o, float3 mx, float3 px, float3 g0, float3 g1,
+                                                float3 g2, float3 g3, float lambda, float d) {
+    if (!f) return o;
+    const int deg = __popc(f);
+    const float fd = (float)deg;
+    const float inv = deg == 1 ? 1.f : deg == 2 ? 0.5f : deg == 3 ? (1.f / 3.f) : deg == 4 ? 0.25f
+                    : deg == 5 ? 0.2f : (1.f / 6.f);
+    const float ex = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
+    const float ey = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
+    const float ez = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
+    return make_float3(jacobi_axis(ex, o.x, mx.x, px.x, g0.x, g1.x, g2.x, g3.x, f, fd, inv, lambda, d),
+                       jacobi_axis(ey, o.y, mx.y, px.y, g0.y, g1.y, g2.y, g3.y, f, fd, inv, lambda, d),
+                       jacobi_axis(ez, o.z, mx.z, px.z, g0.z, g1.z, g2.z, g3.z, f, fd, inv, lambda, d));
+}
+
 // Smoothing cache: from the CSR stencil, a fixed-stride table of
 // the -z,-y,+y,+z neighbour WINDOW indices of every own point (slots of absent
 // faces hold the point itself).  The +-x neighbours need no table: ids are
@@ -120,27 +155,11 @@ __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
         for (int u = 0; u < 2; ++u) {
             if (i[u] >= n) continue;
             const uint32_t fu = f[u];
-            float3 r = o[u];
-            if (fu) {
-                if (src) {
-                    if ((fu & 4u) && lane == 0 && u == 0) mxo[0] = ld3(src, w[u] - 1u);
-                    if ((fu & 8u) && (lane == 31 && u == 1 || i[u] + 1u >= n)) pxo[u] = ld3(src, w[u] + 1u);
-                }
-                const float m0 = (fu & 1u) ? 1.f : 0.f, m1 = (fu & 2u) ? 1.f : 0.f, m2 = (fu & 4u) ? 1.f : 0.f;
-                const float m3 = (fu & 8u) ? 1.f : 0.f, m4 = (fu & 16u) ? 1.f : 0.f, m5 = (fu & 32u) ? 1.f : 0.f;
-                const int deg = __popc(fu);
-                const float fd = (float)deg;
-                // e (face directions) + sum of neighbour offsets - deg * o
-                float sx = (m3 - m2) + (m2 * mxo[u].x + m3 * pxo[u].x + m0 * g[u][0].x + m1 * g[u][1].x + m4 * g[u][2].x + m5 * g[u][3].x) - fd * o[u].x;
-                float sy = (m4 - m1) + (m2 * mxo[u].y + m3 * pxo[u].y + m0 * g[u][0].y + m1 * g[u][1].y + m4 * g[u][2].y + m5 * g[u][3].y) - fd * o[u].y;
-                float sz = (m5 - m0) + (m2 * mxo[u].z + m3 * pxo[u].z + m0 * g[u][0].z + m1 * g[u][1].z + m4 * g[u][2].z + m5 * g[u][3].z) - fd * o[u].z;
-                // m = sum / N (N <= 6: multiply by the fp32 reciprocal), q = o + lambda m, clamp (Q8, Q9)
-                const float inv = deg == 1 ? 1.f : deg == 2 ? 0.5f : deg == 3 ? (1.f / 3.f) : deg == 4 ? 0.25f
-                                : deg == 5 ? 0.2f : (1.f / 6.f);
-                r.x = fminf(fmaxf(__fadd_rn(o[u].x, __fmul_rn(a.lambda, __fmul_rn(sx, inv))), -a.d), a.d);
-                r.y = fminf(fmaxf(__fadd_rn(o[u].y, __fmul_rn(a.lambda, __fmul_rn(sy, inv))), -a.d), a.d);
-                r.z = fminf(fmaxf(__fadd_rn(o[u].z, __fmul_rn(a.lambda, __fmul_rn(sz, inv))), -a.d), a.d);
+            if (fu && src) {
+                if ((fu & 4u) && lane == 0 && u == 0) mxo[0] = ld3(src, w[u] - 1u);
+                if ((fu & 8u) && (lane == 31 && u == 1 || i[u] + 1u >= n)) pxo[u] = ld3(src, w[u] + 1u);
             }
+            const float3 r = jacobi_update(fu, o[u], mxo[u], pxo[u], g[u][0], g[u][1], g[u][2], g[u][3], a.lambda, a.d);
             const uint32_t ww = w[u];
             if (a.world) {
                 a.world[3u * ww + 0u] = world_of(__ldg(a.points + 3u * ww + 0u), r.x, a.org[0], a.sp[0]);

@@ -23,6 +23,7 @@
 #include "k_emit.cuh"
 #include "k_scan.cuh"
 #include "k_smooth.cuh"
+#include "k_smooth_tb.cuh"
 
 using namespace psn;
 
@@ -34,6 +35,9 @@ struct psn_ctx {
     std::vector<uint32_t> label_host;     // bitset or sorted list kept alive for async copies
     // workspaces holding a valid COUNT result, with the volume signature they were counted for
     std::map<const void *, std::array<int64_t, 6>> counted;
+    int smooth_mode = PSN_SMOOTH_PER_ITERATION;   // psn_ctx_set_smoothing (measured faster)
+    int32_t smooth_group = 0;                 // iterations per wavefront launch (0 = automatic)
+    int32_t smooth_tile = 0;                  // points per wavefront tile (0 = automatic)
 };
 
 namespace {
@@ -386,14 +390,19 @@ psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, 
 }
 
 namespace {
-struct SmoothLayout { size_t nbr, buf0, buf1, total; int64_t nw; };
+struct SmoothLayout { size_t nbr, buf0, buf1, rng, done, sch, total; int64_t nw, U; };
+// [nbr uint4 x P | buf0 float4 x W | buf1 float4 x W | rng int2 x U | done u32 x U | sched]
 SmoothLayout smooth_layout(const psn_mesh *m) {
     SmoothLayout L;
     L.nw = m->halo_lo_points + m->n_points + m->halo_hi_points;
+    L.U = (m->n_points + kTbTileMin - 1) / kTbTileMin;   // schedule arrays sized for the smallest tile
     L.nbr = 0;
     L.buf0 = align_up(16 * (size_t)std::max<int64_t>(m->n_points, 1));
-    L.buf1 = L.buf0 + align_up(12 * (size_t)std::max<int64_t>(L.nw, 1));
-    L.total = L.buf1 + align_up(12 * (size_t)std::max<int64_t>(L.nw, 1));
+    L.buf1 = L.buf0 + align_up(16 * (size_t)std::max<int64_t>(L.nw, 1));
+    L.rng = L.buf1 + align_up(16 * (size_t)std::max<int64_t>(L.nw, 1));
+    L.done = L.rng + align_up(8 * (size_t)std::max<int64_t>(L.U, 1));
+    L.sch = L.done + align_up(4 * (size_t)std::max<int64_t>(L.U, 1));
+    L.total = L.sch + align_up(sizeof(TbSched));
     return L;
 }
 }  // namespace
@@ -478,20 +487,81 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         return cuda_check(ctx, "finalize launch");
     }
     if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
-    float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
-    SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
-    for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
-    const float *src = nullptr;
-    for (int32_t t = 0; t < iterations; ++t) {
-        a.src = src;
-        const bool last = (t == iterations - 1);
-        a.dst = last ? nullptr : buf[t & 1];
-        a.world = last ? out : nullptr;
-        k_smooth<<<(unsigned)gs, 256, 0, st>>>(a);
-        ++ctx->launches;
-        src = a.dst;
+    if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
+        // one launch per Jacobi iteration (float3 buffers in the two buffer slots)
+        float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
+        SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
+        for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
+        const float *src = nullptr;
+        for (int32_t t = 0; t < iterations; ++t) {
+            a.src = src;
+            const bool last = (t == iterations - 1);
+            a.dst = last ? nullptr : buf[t & 1];
+            a.world = last ? out : nullptr;
+            k_smooth<<<(unsigned)gs, 256, 0, st>>>(a);
+            ++ctx->launches;
+            src = a.dst;
+        }
+        return cuda_check(ctx, "smooth launch");
     }
-    return cuda_check(ctx, "smooth launch");
+    // wavefront (temporally blocked) smoothing: G iterations per persistent launch
+    TbSched *sch = at<TbSched>(ws, SL.sch);
+    uint32_t *done = at<uint32_t>(ws, SL.done);
+    int2 *rng = at<int2>(ws, SL.rng);
+    const uint32_t tile = ctx->smooth_tile > 0 ? (uint32_t)ctx->smooth_tile : 1024u;
+    const int64_t U = (nw + tile - 1) / tile;
+    if (cudaMemsetAsync(sch, 0, sizeof(TbSched), st) != cudaSuccess ||
+        cudaMemsetAsync(done, 0, 4 * (size_t)U, st) != cudaSuccess)
+        return cuda_check(ctx, "smooth memset");
+    k_tile_ranges<<<(unsigned)U, 256, 0, st>>>(static_cast<const uint4 *>(ws), mesh->face_masks, (uint32_t)nw, tile,
+                                               rng, sch);
+    ++ctx->launches;
+    // iterations per launch: keep the live window (G x ~2 voxel layers of points x 49 B) well inside L2
+    int32_t G = ctx->smooth_group;
+    if (G <= 0) {
+        const double layer_pts = (double)nw / (double)std::max<int64_t>(vol->dims[2] - 1, 1);
+        // window ~ 2G blocks of (one layer ~ neighbour distance) points; ~40 MB of the 126 MB L2
+        G = (int32_t)std::max(1.0, std::min((double)iterations, 40.0e6 / (4.0 * layer_pts * 49.0)));
+    }
+    TbArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    ta.buf[0] = at<float4>(ws, SL.buf0); ta.buf[1] = at<float4>(ws, SL.buf1);
+    ta.world = out; ta.fmask = mesh->face_masks; ta.nbr = static_cast<const uint4 *>(ws); ta.points = mesh->points;
+    ta.rng = rng; ta.done = done; ta.sch = sch;
+    ta.n = (uint32_t)nw; ta.U = (uint32_t)U; ta.tile = tile; ta.T = iterations;
+    ta.lambda = relaxation; ta.d = constraint_distance;
+    for (int c = 0; c < 3; ++c) { ta.sp[c] = vol->spacing[c]; ta.org[c] = vol->origin[c]; }
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, U * iterations));
+    for (int32_t t0 = 0; t0 < iterations; t0 += G) {
+        ta.t0 = t0; ta.G = std::min(G, iterations - t0);
+        if (cudaMemsetAsync(&sch->counter, 0, sizeof(uint32_t), st) != cudaSuccess) return cuda_check(ctx, "smooth memset");
+        k_smooth_tb<<<grid, 256, 0, st>>>(ta);
+        ++ctx->launches;
+    }
+    return cuda_check(ctx, "smooth wavefront launch");
+}
+
+psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, void *stream) {
+    if (!ctx || !mesh || !ws) return PSN_ERR_ARG;
+    const SmoothLayout SL = smooth_layout(mesh);
+    if (ws_bytes < SL.total) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
+    TbSched h;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(&h, static_cast<const char *>(ws) + SL.sch, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return cuda_check(ctx, "smooth status read-back");
+    if (h.error) return fail(ctx, PSN_ERR_CUDA, "wavefront smoothing: a dependency wait timed out");
+    return PSN_OK;
+}
+
+psn_status psn_ctx_set_smoothing(psn_ctx *ctx, int mode, int32_t iterations_per_launch, int32_t points_per_tile) {
+    if (!ctx || (mode != PSN_SMOOTH_WAVEFRONT && mode != PSN_SMOOTH_PER_ITERATION) || iterations_per_launch < 0 ||
+        points_per_tile < 0 || points_per_tile % (int32_t)kTbTileMin != 0)
+        return PSN_ERR_ARG;
+    ctx->smooth_mode = mode;
+    ctx->smooth_group = iterations_per_launch;
+    ctx->smooth_tile = points_per_tile;
+    return PSN_OK;
 }
 
 psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, const float *src,

@@ -223,3 +223,30 @@ def test_wide_rows_multi_xtile():
     _check_volume(a, T=3)
     a = rng.integers(0, 3, size=(3, 4, 4500)).astype(np.uint8)
     _check_volume(a, T=2)
+
+
+@pytest.mark.parametrize("G,tile", [(0, 0), (1, 256), (3, 512), (7, 2048)])
+def test_wavefront_smoothing_bit_identical(G, tile):
+    """psn_smooth's wavefront (temporally blocked) schedule == one launch per iteration, bit for bit,
+    and within 1e-4 x spacing of the fp64 oracle."""
+    p = gu.psn()
+    rng = np.random.default_rng(31 + G)
+    vols = [rng.integers(0, 4, size=(30, 40, 50)).astype(np.uint8),
+            psn_gen.generate_host(psn_gen.config("c2"))[:80]]
+    try:
+        for a in vols:
+            _, vol, mesh, _ = gu.gpu_extract(a, spacing=(0.8, 1.0, 1.5))
+            T = 11
+            ws = p.smooth_workspace(mesh)
+            p.set_smoothing(1, 0)
+            ref = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()
+            p.set_smoothing(0, G, tile)
+            out = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws)
+            p.smooth_status(mesh, ws)
+            np.testing.assert_array_equal(out[:mesh.n_points].cpu().numpy(), ref[:mesh.n_points].cpu().numpy())
+            om = oracle.extract(oracle.as_volume(a, (0.8, 1.0, 1.5)))
+            o64 = oracle.smooth(om, (0.8, 1.0, 1.5), T, 0.5, 0.5)
+            err = np.abs(out[:mesh.n_points].cpu().numpy().astype(np.float64) - o64) / np.array((0.8, 1.0, 1.5))
+            assert err.max() <= TOL
+    finally:
+        p.set_smoothing(1, 0, 0)
