@@ -197,6 +197,15 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, s
 enum { PSN_SMOOTH_WAVEFRONT = 0, PSN_SMOOTH_PER_ITERATION = 1 };
 psn_status psn_ctx_set_smoothing(psn_ctx *ctx, int mode, int32_t iterations_per_launch, int32_t points_per_tile);
 
+/* Counting kernel of psn_extract(PSN_COUNT) (Passes 1-3):
+ *   PSN_COUNT_AUTO (default): the warp-per-row producer/consumer kernel
+ *     (k_count3) when a voxel row fits one warp (M-1 <= 256*16/b, b = label
+ *     bytes; u32: M-1 <= 512), else the x-tiled kernel (k_count).
+ *   PSN_COUNT_XTILE: always the x-tiled kernel.
+ * Both produce identical counts and point planes (tested). */
+enum { PSN_COUNT_AUTO = 0, PSN_COUNT_XTILE = 1 };
+psn_status psn_ctx_set_counting(psn_ctx *ctx, int mode);
+
 /* Synchronising check of the last psn_smooth on ws: PSN_ERR_CUDA if a
  * wavefront dependency wait timed out (a guard that must never trigger). */
 psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, void *stream);

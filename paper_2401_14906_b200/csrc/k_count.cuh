@@ -51,6 +51,8 @@ struct CountArgs {
     LabelSet ls;
     int multi_xt;              // several x-tiles per row: accumulate with global atomics
     int tma;                   // rows are 16-byte aligned: stage with cp.async.bulk
+    int probe;                 // k_count3 experiment: 1 = consumers only wait/release (memory pipeline alone)
+    int NS;                    // k_count3 ring slots
 };
 
 template <typename T> __host__ __device__ constexpr int count_tj() { return 4; }

@@ -1,0 +1,425 @@
+// k_count3.cuh -- Passes 1-3 (counting half) of PSN extraction, warp-per-row
+// producer/consumer variant for rows that fit one warp (M-1 <= 256*E).
+//
+// PAPER sec 2.3: Pass 1 classifies x-edges and trims rows, Pass 2
+// classifies y/z-edges, Pass 3 combines them into the per-voxel
+// edge case and the point / quad / stencil counts of each voxel row (P:85-86,
+// P:118).  Here all three run in one z-marching kernel:
+//
+//   CTA      = kC3Rows voxel rows (j0 .. j0+7) x the full row, marching over a
+//              z-chunk of voxel layers [kbeg, kend).
+//   producer = one warp that streams the kC3Rows+1 grid rows of each lattice
+//              slice into a shared-memory ring with TMA bulk copies
+//              (cp.async.bulk, completion on a FULL mbarrier per slot) and
+//              refills a slot once every consumer warp has arrived on its
+//              EMPTY mbarrier.  No __syncthreads in the main loop.
+//   consumer = one warp per voxel row; lane = 16-byte CHUNK(s) of E = 16/b
+//              x positions (CPL chunks per lane).
+//
+// Per grid row, slice and chunk a KEY is computed once: the label value if all
+// E+1 elements (the chunk plus the next one) are equal, else a tag that can
+// equal neither a value nor the tags of the other three grid rows of a voxel
+// row.  A voxel-row chunk has no intersected edge -- no point -- iff its four
+// keys (rows j, j+1 at slices k, k+1) are equal: the GPU form of the paper's
+// computational trimming ("rapidly skip portions of rows, entire
+// rows, and even entire data slices").  Keys of slice k+1 are reused as the
+// keys of slice k at the next layer.  The non-uniform chunks are compacted
+// into a per-warp queue (ballot + popc) and processed 32 at a time with full
+// lanes by the SWAR slow path, which forms the six face planes c^f,
+// the point plane (c^e != 0) and the owned-quad / stencil counts.
+//
+// Outputs per voxel row r = j + (N-1)(k - kA): cntP/cntQ/cntS (halo layers
+// count points only) and, for rows with >= 1 point, the point bit-plane
+// pmask[r][w] (bit b of word w <-> voxel 32w + b) and ppre[r][w], the number
+// of points of the row before word w (the row iterator's running id).
+// Rows without points leave pmask/ppre unwritten: Pass 4 never reads them.
+#pragma once
+#include <type_traits>
+#include "k_count.cuh"
+#include "psn_common.cuh"
+
+namespace psn {
+
+constexpr int kC3Rows = 8;                       // consumer warps = voxel rows per CTA
+constexpr int kC3MaxStages = 8;                  // ring slots (lattice slices): CountArgs.NS <= this
+constexpr int kC3Threads = 32 * (kC3Rows + 1);   // + one producer warp
+
+template <typename T> struct KeyOf { using type = uint32_t; };
+template <> struct KeyOf<uint32_t> { using type = unsigned long long; };
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Key of the chunk at shared address `addr` (E elements + the next one).  At
+// the row end the staged row is padded with copies of element M-1, so the
+// elements past the row never make a chunk non-uniform.
+template <typename T, bool ANZ>
+__device__ __forceinline__ typename KeyOf<T>::type chunk_key(uint32_t addr, uint32_t tag, const LabelSet &ls) {
+    constexpr int NW = Pack<T>::NW;
+    uint32_t w[NW];
+    lds_chunk<T>(addr, w);
+    uint32_t nx = lds32(addr + 16);
+    if (!ANZ) { remap<T>(ls, w); nx = remap1<T>(ls, nx); }
+    uint32_t v, d = (w[0] ^ w[1]) | (w[0] ^ w[2]) | (w[0] ^ w[3]);   // the four words are equal ...
+    if constexpr (sizeof(T) == 1) {
+        v = w[0] & 0xFFu;
+        d |= ((w[0] ^ (w[0] >> 8)) & 0x00FFFFFFu) | ((nx ^ w[0]) & 0xFFu);
+    } else if constexpr (sizeof(T) == 2) {
+        v = w[0] & 0xFFFFu;
+        d |= ((w[0] ^ (w[0] >> 16)) | (nx ^ w[0])) & 0xFFFFu;
+    } else {
+        v = w[0];
+        d |= nx ^ w[0];                                           // ... and so are a word's elements and the next
+    }
+    const bool nonconst = d != 0u;
+    if constexpr (sizeof(T) == 4) return nonconst ? ((1ull << 32) | tag) : (unsigned long long)v;
+    else return nonconst ? (0x80000000u | tag) : v;
+}
+
+// Pad a staged row (M elements at shared address `row`) with copies of its
+// last element: 32 bytes from byte offset M*b (16-byte aligned when staged by
+// TMA).  Two warps may pad the same row; they write the same bytes.
+template <typename T>
+__device__ __forceinline__ void pad_row(uint32_t row, int64_t M) {
+    const uint32_t end = row + (uint32_t)(M * (int64_t)sizeof(T));
+    uint32_t v;
+    if constexpr (sizeof(T) == 1) { uint32_t x; asm volatile("ld.shared.u8 %0, [%1];" : "=r"(x) : "r"(end - 1)); v = x * 0x01010101u; }
+    else if constexpr (sizeof(T) == 2) { uint32_t x; asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(end - 2)); v = x * 0x00010001u; }
+    else v = lds32(end - 4);
+    if ((end & 15u) == 0u) {
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(end), "r"(v) : "memory");
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(end + 16), "r"(v) : "memory");
+    } else {   // rows staged by the copy fallback (M*b not a multiple of 16)
+        for (uint32_t b = 0; b < 32; b += sizeof(T)) {
+            if constexpr (sizeof(T) == 1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(end + b), "r"(v) : "memory");
+            else if constexpr (sizeof(T) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(end + b), "r"(v) : "memory");
+            else asm volatile("st.shared.u32 [%0], %1;" ::"r"(end + b), "r"(v) : "memory");
+        }
+    }
+}
+
+// Spread-form "element differs" flag planes of t = XOR-combinations of chunk
+// words: one flag per element slot.  u16 uses the 16x2 SIMD min (VIMNMX):
+// min(t_e, 1) puts the flag in bit 0 of each half; u8 / u32 use the carry
+// trick ((t & LOW) + LOW) | t, which puts it in the MSB of each slot.
+template <typename T> struct Flags {
+    static constexpr bool LOWBIT = sizeof(T) == 2;
+    static constexpr uint32_t FL = LOWBIT ? 0x00010001u : Pack<T>::MSB;   // flag bit of every slot
+    static constexpr int POS0 = LOWBIT ? 0 : Pack<T>::EB - 1;             // flag bit within a slot
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t nz(uint32_t t) {
+    if constexpr (Flags<T>::LOWBIT) return __vminu2(t, 0x00010001u);
+    else return ((t & Pack<T>::LOW) + Pack<T>::LOW) | t;
+}
+
+// Append flag plane p (masked to flag bits by the caller) to a packed counter
+// word: planes occupy distinct bits next to each slot's flag bit.
+template <typename T>
+__device__ __forceinline__ uint32_t pack(uint32_t acc, uint32_t p) {
+    if constexpr (Flags<T>::LOWBIT) return (acc << 1) | p;
+    else return (acc >> 1) | p;
+}
+
+// Compress the flags of one word to EPW contiguous bits.
+template <typename T>
+__device__ __forceinline__ uint32_t movemask(uint32_t w) {
+    if constexpr (sizeof(T) == 1) return (((w >> 7) & 0x01010101u) * 0x01020408u) >> 24;
+    else if constexpr (sizeof(T) == 2) { const uint32_t x = w & 0x10001u; return (x | (x >> 15)) & 3u; }
+    else return w >> 31;
+}
+
+// Slow path of one voxel-row chunk: A/B = grid rows j/j+1 of slice k, C/D of
+// slice k+1 (shared addresses of the chunk).  Returns the E point bits and
+// adds the owned quads (open boundaries P:264) and directed stencil
+// entries of the chunk's voxels to cq / cs.
+struct SlowCtx {
+    int64_t M;
+    uint32_t mz, my, mpy, mpz;   // MSB masks of the warp-uniform face conditions (k>=1, j>=1, j<=N-3, k<=O-3)
+    uint32_t mqx, mqy, mqz;      // owned-quad conditions (j>=1&&k>=1, k>=1, j>=1)
+    bool own;
+};
+
+template <typename T, bool ANZ>
+__device__ __forceinline__ uint32_t slow_chunk(uint32_t aA, uint32_t aB, uint32_t aC, uint32_t aD, int xc,
+                                               const SlowCtx &sc, const LabelSet &ls, uint32_t &cq, uint32_t &cs) {
+    constexpr int NW = Pack<T>::NW, E = Pack<T>::E, EB = Pack<T>::EB, EPW = Pack<T>::EPW;
+    constexpr uint32_t FL = Flags<T>::FL;
+    uint32_t A[NW], B[NW], C[NW], D[NW], nA, nB, nC, nD;
+    lds_chunk<T>(aA, A); nA = lds32(aA + 16);
+    lds_chunk<T>(aB, B); nB = lds32(aB + 16);
+    lds_chunk<T>(aC, C); nC = lds32(aC + 16);
+    lds_chunk<T>(aD, D); nD = lds32(aD + 16);
+    if (!ANZ) {
+        remap<T>(ls, A); remap<T>(ls, B); remap<T>(ls, C); remap<T>(ls, D);
+        nA = remap1<T>(ls, nA); nB = remap1<T>(ls, nB); nC = remap1<T>(ls, nC); nD = remap1<T>(ls, nD);
+    }
+    uint32_t hA[NW], hB[NW], hC[NW], hD[NW];
+    shift1<T>(A, nA, hA); shift1<T>(B, nB, hB); shift1<T>(C, nC, hC); shift1<T>(D, nD, hD);
+    // voxel-validity masks: interior chunks (the common case) need no per-element work
+    uint32_t mvox[NW], mi1[NW], miM3[NW];
+    if (xc >= 1 && (int64_t)xc + E + 2 <= sc.M) {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) { mvox[q] = FL; mi1[q] = FL; miM3[q] = FL; }
+    } else {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) { mvox[q] = 0; mi1[q] = 0; miM3[q] = 0; }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint32_t bit = 1u << ((EB * (e % EPW) + Flags<T>::POS0) & 31);
+            const int64_t i = xc + e;
+            if (i <= sc.M - 2) mvox[e / EPW] |= bit;
+            if (i >= 1) mi1[e / EPW] |= bit;
+            if (i <= sc.M - 3) miM3[e / EPW] |= bit;
+        }
+    }
+    uint32_t bits = 0, qacc = 0, sacc = 0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+        const uint32_t a = A[q], b = B[q], c = C[q], d = D[q], ha = hA[q], hb = hB[q], hc = hC[q], hd = hD[q];
+        const uint32_t xa = a ^ ha, yab = a ^ b, zac = a ^ c;
+        const uint32_t Fmx = nz<T>(yab | zac | (a ^ d));          // face x=i   : corners A B C D
+        const uint32_t Fpx = nz<T>((ha ^ hb) | (ha ^ hc) | (ha ^ hd));
+        const uint32_t Fmy = nz<T>(xa | zac | (a ^ hc));          // face y=j   : A hA C hC
+        const uint32_t Fpy = nz<T>((b ^ hb) | (b ^ d) | (b ^ hd));
+        const uint32_t Fmz = nz<T>(xa | yab | (a ^ hb));          // face z=k   : A hA B hB
+        const uint32_t Fpz = nz<T>((c ^ hc) | (c ^ d) | (c ^ hd));
+        const uint32_t pt = (Fmx | Fpx | Fmy | Fpy) & mvox[q];    // each edge lies on one of these faces
+        bits |= movemask<T>(pt) << (q * EPW);
+        if (sc.own) {
+            const uint32_t mv = mvox[q];
+            // directed stencil entries: faces whose neighbour voxel exists
+            uint32_t s = Fmz & mv & sc.mz;
+            s = pack<T>(s, Fmy & mv & sc.my);
+            s = pack<T>(s, Fmx & mv & mi1[q]);
+            s = pack<T>(s, Fpx & miM3[q]);
+            s = pack<T>(s, Fpy & mv & sc.mpy);
+            s = pack<T>(s, Fpz & mv & sc.mpz);
+            sacc += __popc(s);
+            // owned quads: x at (j>=1, k>=1), y at (i>=1, k>=1), z at (i>=1, j>=1)
+            uint32_t u = nz<T>(xa) & mv & sc.mqx;
+            u = pack<T>(u, nz<T>(yab) & mv & mi1[q] & sc.mqy);
+            u = pack<T>(u, nz<T>(zac) & mv & mi1[q] & sc.mqz);
+            qacc += __popc(u);
+        }
+    }
+    cq += qacc;
+    cs += sacc;
+    return bits;
+}
+
+template <typename T, bool ANZ, int CPL, int RPW>
+__global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a) {
+    using Key = typename KeyOf<T>::type;
+    constexpr int E = Pack<T>::E, TJ = kC3Rows, NWC = TJ / RPW;
+    using QItem = typename std::conditional<(CPL <= 4), uint8_t, uint16_t>::type;   // (row << log2(32*CPL)) | chunk
+    constexpr int CB = (CPL <= 4) ? 7 : 8;
+    const int NS = a.NS;
+    constexpr int WPL = (CPL * E + 31) / 32;     // mask words per lane
+    constexpr uint32_t MSB = Flags<T>::FL;   // flag bits of the slow path's planes
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ __align__(8) uint64_t full[kC3MaxStages], empty[kC3MaxStages];
+    __shared__ QItem wq[NWC][RPW * 32 * CPL];   // one layer's non-uniform (row, chunk) items
+    __shared__ uint32_t wm[TJ][32 * WPL];
+    __shared__ uint32_t sbits[ANZ ? 1 : 2048];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t M = a.M, N = a.N, NV = N - 1;
+    const int64_t jb = blockIdx.x % a.nJB, zc = blockIdx.x / a.nJB;
+    const int64_t j0 = jb * TJ;
+    const int64_t kbeg = a.kA + zc * a.KZ;
+    const int64_t kend = min(kbeg + a.KZ, a.kB);
+    const int nrows = (int)min((int64_t)TJ, NV - j0);
+    const int nwarps = (nrows + RPW - 1) / RPW;   // active consumer warps
+    const int64_t nsteps = kend - kbeg;
+    const uint32_t RB = (uint32_t)a.RB, SB = (TJ + 1) * RB;
+    const uint32_t sbase = smem_u32(dsm);
+    const uint32_t copy_bytes = (uint32_t)(M * (int64_t)sizeof(T));
+
+    LabelSet ls = a.ls;
+    if (!ANZ && sizeof(T) < 4) {
+        for (int t = tid; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
+        ls.bits = sbits;
+    }
+    for (int t = tid; t < TJ * 32 * WPL; t += blockDim.x) (&wm[0][0])[t] = 0u;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], a.tma ? 1u : 32u);
+            mbar_init(&empty[s], (uint32_t)max(nwarps, 1));
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (nsteps <= 0 || nrows <= 0) return;
+    const T *lab = reinterpret_cast<const T *>(a.labels);
+
+    if (warp == NWC) {
+        // ------------------------------------------------------------ producer
+        int slot = 0;
+        uint32_t ph = 0;   // parity of the slot's refill round
+        for (int64_t s = 0; s <= nsteps; ++s) {
+            if (s >= NS) mbar_wait(&empty[slot], ph ^ 1u);
+            const int64_t z = kbeg + s - a.z_lo;
+            uint8_t *dst = dsm + (uint32_t)slot * SB;
+            if (a.tma) {
+                if (lane == 0) mbar_expect_tx(&full[slot], copy_bytes * (TJ + 1));
+                __syncwarp();
+                if (lane <= TJ) {
+                    fence_proxy_async();
+                    const int64_t j = min(j0 + lane, N - 1);
+                    tma_load_1d(dst + lane * RB, lab + (z * N + j) * M, copy_bytes, &full[slot]);
+                }
+            } else {
+                for (int g = 0; g <= TJ; ++g) {
+                    const int64_t j = min(j0 + g, N - 1);
+                    const T *src = lab + (z * N + j) * M;
+                    T *d = reinterpret_cast<T *>(dst + g * RB);
+                    for (int64_t x = lane; x < M; x += 32) d[x] = src[x];
+                }
+                mbar_arrive(&full[slot]);
+            }
+            if (++slot == NS) { slot = 0; ph ^= 1u; }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int w = warp;
+    if (w >= nwarps) return;
+    const int r0 = w * RPW;                       // first CTA row of this warp
+    const int64_t jw = j0 + r0;
+    const int CPR = (int)((M - 1 + E - 1) / E);   // chunks per row
+    const uint32_t lt = (1u << lane) - 1u;
+    auto keys_of = [&](int64_t s, int slot, Key (&kk)[RPW + 1][CPL]) {
+        const uint32_t tagz = (uint32_t)(s & 1) << 1;
+        const uint32_t sl = sbase + (uint32_t)slot * SB + (uint32_t)r0 * RB;
+        if (lane <= RPW) pad_row<T>(sl + (uint32_t)lane * RB, M);
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g <= RPW; ++g) {
+            const uint32_t base = sl + (uint32_t)g * RB;
+            const uint32_t tag = (uint32_t)(g & 1) | tagz;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = lane + 32 * q;
+                kk[g][q] = (c < CPR) ? chunk_key<T, ANZ>(base + (uint32_t)c * 16u, tag, ls) : Key(0);
+            }
+        }
+    };
+
+    mbar_wait(&full[0], 0u);
+    Key kc[RPW + 1][CPL];
+    keys_of(0, 0, kc);
+    uint32_t qt = 0;
+    int slot0 = 0, slot1 = NS > 1 ? 1 : 0;   // ring slots of slices o and o+1
+    uint32_t ph1 = NS > 1 ? 0u : 1u;          // fill parity of slice o+1's slot
+    for (int64_t o = 0; o < nsteps; ++o) {
+        const int64_t s1 = o + 1;
+        mbar_wait(&full[slot1], ph1);
+        Key kn[RPW + 1][CPL];
+        keys_of(s1, slot1, kn);
+        const int64_t k = kbeg + o;
+        SlowCtx sc;
+        sc.M = M;
+        sc.own = (k >= a.own_k0) && (k < a.own_k1);
+        sc.mz = (k >= 1) ? MSB : 0u;
+        sc.mpz = (k <= a.O - 3) ? MSB : 0u;
+        sc.mqy = sc.mz;
+        const uint32_t a0 = sbase + (uint32_t)slot0 * SB + (uint32_t)r0 * RB;
+        const uint32_t a1 = sbase + (uint32_t)slot1 * SB + (uint32_t)r0 * RB;
+        uint32_t rq[RPW], rs[RPW], dirty = 0;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) { rq[i] = 0; rs[i] = 0; }
+        // classify: every non-uniform (row, chunk) of the layer goes to the warp's queue
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                const int c = lane + 32 * q;
+                const Key x = kc[i][q];
+                const bool nu = (c < CPR) && (r0 + i < nrows) &&
+                                ((x != kc[i + 1][q]) | (x != kn[i][q]) | (x != kn[i + 1][q]));
+                const uint32_t bal = __ballot_sync(kFull, nu);
+                if (nu) wq[w][qt + __popc(bal & lt)] = (QItem)((i << CB) | c);
+                qt += __popc(bal);
+                dirty |= (bal ? 1u : 0u) << i;
+            }
+        }
+        __syncwarp();
+        // slow path: 32 items per round with full lanes (one call site: the body is large)
+        for (uint32_t qh = 0; qh < qt; qh += 32u) {
+            uint32_t cq = 0, cs = 0;
+            int ri = -1;
+            if (qh + lane < qt) {
+                const uint32_t item = wq[w][qh + lane];
+                ri = (int)(item >> CB);
+                const int c = (int)(item & ((1u << CB) - 1u));
+                const int64_t j = jw + ri;
+                SlowCtx sj = sc;
+                sj.my = (j >= 1) ? MSB : 0u;
+                sj.mpy = (j <= N - 3) ? MSB : 0u;
+                sj.mqz = sj.my;
+                sj.mqx = (j >= 1 && k >= 1) ? MSB : 0u;
+                const uint32_t off = (uint32_t)ri * RB + (uint32_t)c * 16u;
+                const uint32_t bits = slow_chunk<T, ANZ>(a0 + off, a0 + RB + off, a1 + off, a1 + RB + off, c * E, sj,
+                                                         ls, cq, cs);
+                if (bits) atomicOr(&wm[r0 + ri][(c * E) >> 5], bits << ((c * E) & 31));
+            }
+            if (sc.own) {
+#pragma unroll
+                for (int i = 0; i < RPW; ++i) {
+                    rq[i] += __reduce_add_sync(kFull, ri == i ? cq : 0u);
+                    rs[i] += __reduce_add_sync(kFull, ri == i ? cs : 0u);
+                }
+            }
+        }
+        qt = 0;
+        __syncwarp();
+        // flush the layer's rows: counts always, point planes only when non-empty
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            if (r0 + i >= nrows) break;
+            const int64_t rr = jw + i + NV * (k - a.kA);
+            if (!((dirty >> i) & 1u)) {
+                if (lane == 0) { a.cntP[rr] = 0u; a.cntQ[rr] = 0u; a.cntS[rr] = 0u; }
+                continue;
+            }
+            uint32_t wv[WPL], cnt = 0;
+#pragma unroll
+            for (int q = 0; q < WPL; ++q) { wv[q] = wm[r0 + i][lane * WPL + q]; cnt += __popc(wv[q]); }
+            const uint32_t P = __reduce_add_sync(kFull, cnt);
+            if (lane == 0) { a.cntP[rr] = P; a.cntQ[rr] = rq[i]; a.cntS[rr] = rs[i]; }
+            if (P) {
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                uint32_t pre = incl - cnt;
+                uint32_t *pm = a.pmask + rr * a.W32;
+                uint16_t *pp = a.ppre + rr * a.W32;
+#pragma unroll
+                for (int q = 0; q < WPL; ++q) {
+                    const int wi = lane * WPL + q;
+                    if (wi < a.W32) { pm[wi] = wv[q]; pp[wi] = (uint16_t)pre; }
+                    pre += __popc(wv[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < WPL; ++q) wm[r0 + i][lane * WPL + q] = 0u;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot0]);   // slice o is no longer read by this warp
+        slot0 = slot1;
+        if (++slot1 == NS) { slot1 = 0; ph1 ^= 1u; }
+#pragma unroll
+        for (int g = 0; g <= RPW; ++g)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) kc[g][q] = kn[g][q];
+    }
+}
+
+}  // namespace psn

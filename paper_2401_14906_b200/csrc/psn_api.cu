@@ -15,11 +15,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "psn.h"
 #include "k_count.cuh"
+#include "k_count3.cuh"
 #include "k_emit.cuh"
 #include "k_scan.cuh"
 #include "k_smooth.cuh"
@@ -38,6 +40,7 @@ struct psn_ctx {
     int smooth_mode = PSN_SMOOTH_PER_ITERATION;   // psn_ctx_set_smoothing (measured faster)
     int32_t smooth_group = 0;                 // iterations per wavefront launch (0 = automatic)
     int32_t smooth_tile = 0;                  // points per wavefront tile (0 = automatic)
+    int count_mode = PSN_COUNT_AUTO;          // psn_ctx_set_counting
 };
 
 namespace {
@@ -169,6 +172,38 @@ cudaError_t launch_count(const CountArgs &ca, int64_t blocks, int threads, size_
     return cudaGetLastError();
 }
 
+template <typename T, bool ANZ, int CPL, int RPW>
+cudaError_t launch_count3(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
+    static size_t attr_set = 0;
+    if (smem > attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_count3<T, ANZ, CPL, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = smem;
+    }
+    k_count3<T, ANZ, CPL, RPW><<<(unsigned)blocks, 32 * (kC3Rows / RPW + 1), smem, st>>>(ca);
+    return cudaGetLastError();
+}
+
+template <typename T, bool ANZ, int RPW>
+cudaError_t dispatch_count3_cpl(const CountArgs &ca, int cpl, int64_t blocks, size_t smem, cudaStream_t st) {
+    switch (cpl) {
+        case 1: return launch_count3<T, ANZ, 1, RPW>(ca, blocks, smem, st);
+        case 2: return launch_count3<T, ANZ, 2, RPW>(ca, blocks, smem, st);
+        case 4: return launch_count3<T, ANZ, 4, RPW>(ca, blocks, smem, st);
+        default:
+            if constexpr (sizeof(T) < 4) return launch_count3<T, ANZ, 8, RPW>(ca, blocks, smem, st);
+            return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T>
+cudaError_t dispatch_count3(const CountArgs &ca, bool anz, int cpl, int64_t blocks, size_t smem, cudaStream_t st) {
+    constexpr int RPW = 2;   // voxel rows per consumer warp (measured: c3/c5b faster than 1, c4 equal; 4 slower)
+    return anz ? dispatch_count3_cpl<T, true, RPW>(ca, cpl, blocks, smem, st)
+               : dispatch_count3_cpl<T, false, RPW>(ca, cpl, blocks, smem, st);
+}
+
 template <typename T>
 cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int threads, size_t smem, cudaStream_t st) {
     return anz ? launch_count<T, true>(ca, blocks, threads, smem, st) : launch_count<T, false>(ca, blocks, threads, smem, st);
@@ -282,48 +317,80 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         if (cudaMemsetAsync(at<char>(ws, L.hdr), 0, L.cntP - L.hdr, st) != cudaSuccess) return cuda_check(ctx, "memset");
         const int64_t E = 16 / eb;                            // elements per 16-byte lane chunk
         const int64_t chunks = (L.M - 1 + E - 1) / E;        // lane chunks per row
-        const int64_t nXT = (chunks + 255) / 256;             // 256 chunks (256*E x-positions) per CTA
-        const int64_t WX = std::min<int64_t>((chunks + 31) / 32, 8);
-        const int tj = eb == 1 ? count_tj<uint8_t>() : (eb == 2 ? count_tj<uint16_t>() : count_tj<uint32_t>());
-        const int64_t nJB = (L.N - 1 + tj - 1) / tj;
         const int64_t nLay = L.kB - L.kA;
-        // z-chunks: ~8 waves of CTAs (4 resident per SM) so the last wave's tail is small,
-        // while each CTA still marches >= 16 layers to amortise its TMA prologue
-        const int64_t target_ctas = (int64_t)ctx->sms * 4 * 8;
-        int64_t nZC = std::max<int64_t>(1, (target_ctas + nXT * nJB - 1) / (nXT * nJB));
-        nZC = std::min(nZC, std::max<int64_t>(1, nLay / 16));
-        nZC = std::min(nZC, nLay);
-        const int64_t KZ = (nLay + nZC - 1) / nZC;
-        nZC = (nLay + KZ - 1) / KZ;
-        const int64_t xpad = 16 / eb;
-        // every thread of the CTA reads its 16-byte chunk and the next word, so a staged row
-        // spans the CTA's full width (zero-filled past the row end), plus the 16-byte pad
-        const int64_t RB = (int64_t)align16((size_t)((32 * WX * E + xpad) * eb));
-        const size_t smem = (size_t)kCountStages * (size_t)(tj + 1) * (size_t)RB;
+        const int cpl_max = eb == 4 ? 4 : 8;
+        int cpl = 1;
+        while (cpl < cpl_max && 32 * cpl < chunks) cpl *= 2;
+        const bool use3 = ctx->count_mode == PSN_COUNT_AUTO && chunks <= 32 * cpl;
         CountArgs ca;
         ca.labels = slab0; ca.M = L.M; ca.N = L.N; ca.O = L.O; ca.z_lo = vol->z_lo;
         ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W32 = L.W32;
-        ca.nXT = nXT; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB;
         ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
         ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask); ca.ppre = at<uint16_t>(ws, L.ppre);
-        ca.ls = ls; ca.multi_xt = nXT > 1 ? 1 : 0;
+        ca.ls = ls;
+        ca.probe = 0;
         ca.tma = ((L.M * eb) % 16 == 0) && ((reinterpret_cast<uintptr_t>(slab0) & 15u) == 0);
-        const int64_t gridR = std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8);
-        if (ca.multi_xt) {
-            k_init_multixt<<<(unsigned)gridR, 256, 0, st>>>(ca.cntP, ca.cntQ, ca.cntS, ca.trim, L.R);
-            ++ctx->launches;
-        }
-        const int64_t blocks = nXT * nJB * nZC;
-        const int threads = (int)(32 * WX);
         cudaError_t ce;
-        if (eb == 1) ce = dispatch_count<uint8_t>(ca, anz, blocks, threads, smem, st);
-        else if (eb == 2) ce = dispatch_count<uint16_t>(ca, anz, blocks, threads, smem, st);
-        else ce = dispatch_count<uint32_t>(ca, anz, blocks, threads, smem, st);
-        if (ce != cudaSuccess) return fail(ctx, PSN_ERR_CUDA, "k_count launch: %s", cudaGetErrorString(ce));
-        ++ctx->launches;
-        if (ca.multi_xt) {
-            k_trim_fix<<<(unsigned)gridR, 256, 0, st>>>(ca.trim, ca.cntP, L.R);
+        if (use3) {
+            // warp-per-row producer/consumer kernel: 8 voxel rows per CTA, z-chunks sized for
+            // ~8 waves of 2 CTAs per SM, each CTA marching >= 16 layers
+            const int64_t nJB = (L.N - 1 + kC3Rows - 1) / kC3Rows;
+            const int64_t target_ctas = (int64_t)ctx->sms * 2 * 8;
+            int64_t nZC = std::max<int64_t>(1, (target_ctas + nJB - 1) / nJB);
+            nZC = std::min(nZC, std::max<int64_t>(1, nLay / 16));
+            nZC = std::min(nZC, nLay);
+            const int64_t KZ = (nLay + nZC - 1) / nZC;
+            nZC = (nLay + KZ - 1) / KZ;
+            const int64_t RB = (int64_t)align16((size_t)(L.M * eb)) + 32;   // row + 32-byte pad (pad_row)
+            // ring depth: as many slices as keep 3 CTAs resident per SM (<= ~70 KB each), 3..8
+            const int64_t SBy = (int64_t)(kC3Rows + 1) * RB;
+            int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, (70 * 1024) / SBy));
+            if (const char *e = getenv("PSN_COUNT_NS")) ns = std::max(3, std::min(kC3MaxStages, atoi(e)));
+            const size_t smem = (size_t)ns * (size_t)(kC3Rows + 1) * (size_t)RB;
+            ca.NS = ns;
+            ca.nXT = 1; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB; ca.multi_xt = 0;
+            const int64_t blocks = nJB * nZC;
+            if (eb == 1) ce = dispatch_count3<uint8_t>(ca, anz, cpl, blocks, smem, st);
+            else if (eb == 2) ce = dispatch_count3<uint16_t>(ca, anz, cpl, blocks, smem, st);
+            else ce = dispatch_count3<uint32_t>(ca, anz, cpl, blocks, smem, st);
+            if (ce != cudaSuccess) return fail(ctx, PSN_ERR_CUDA, "k_count3 launch: %s", cudaGetErrorString(ce));
             ++ctx->launches;
+        } else {
+            const int64_t nXT = (chunks + 255) / 256;             // 256 chunks (256*E x-positions) per CTA
+            const int64_t WX = std::min<int64_t>((chunks + 31) / 32, 8);
+            const int tj = eb == 1 ? count_tj<uint8_t>() : (eb == 2 ? count_tj<uint16_t>() : count_tj<uint32_t>());
+            const int64_t nJB = (L.N - 1 + tj - 1) / tj;
+            // z-chunks: ~8 waves of CTAs (4 resident per SM) so the last wave's tail is small,
+            // while each CTA still marches >= 16 layers to amortise its TMA prologue
+            const int64_t target_ctas = (int64_t)ctx->sms * 4 * 8;
+            int64_t nZC = std::max<int64_t>(1, (target_ctas + nXT * nJB - 1) / (nXT * nJB));
+            nZC = std::min(nZC, std::max<int64_t>(1, nLay / 16));
+            nZC = std::min(nZC, nLay);
+            const int64_t KZ = (nLay + nZC - 1) / nZC;
+            nZC = (nLay + KZ - 1) / KZ;
+            const int64_t xpad = 16 / eb;
+            // every thread of the CTA reads its 16-byte chunk and the next word, so a staged row
+            // spans the CTA's full width (zero-filled past the row end), plus the 16-byte pad
+            const int64_t RB = (int64_t)align16((size_t)((32 * WX * E + xpad) * eb));
+            const size_t smem = (size_t)kCountStages * (size_t)(tj + 1) * (size_t)RB;
+            ca.nXT = nXT; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB;
+            ca.multi_xt = nXT > 1 ? 1 : 0;
+            const int64_t gridR = std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8);
+            if (ca.multi_xt) {
+                k_init_multixt<<<(unsigned)gridR, 256, 0, st>>>(ca.cntP, ca.cntQ, ca.cntS, ca.trim, L.R);
+                ++ctx->launches;
+            }
+            const int64_t blocks = nXT * nJB * nZC;
+            const int threads = (int)(32 * WX);
+            if (eb == 1) ce = dispatch_count<uint8_t>(ca, anz, blocks, threads, smem, st);
+            else if (eb == 2) ce = dispatch_count<uint16_t>(ca, anz, blocks, threads, smem, st);
+            else ce = dispatch_count<uint32_t>(ca, anz, blocks, threads, smem, st);
+            if (ce != cudaSuccess) return fail(ctx, PSN_ERR_CUDA, "k_count launch: %s", cudaGetErrorString(ce));
+            ++ctx->launches;
+            if (ca.multi_xt) {
+                k_trim_fix<<<(unsigned)gridR, 256, 0, st>>>(ca.trim, ca.cntP, L.R);
+                ++ctx->launches;
+            }
         }
         ScanArgs sa;
         sa.cntP = ca.cntP; sa.cntQ = ca.cntQ; sa.cntS = ca.cntS;
@@ -551,6 +618,12 @@ psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws,
         cudaStreamSynchronize(st) != cudaSuccess)
         return cuda_check(ctx, "smooth status read-back");
     if (h.error) return fail(ctx, PSN_ERR_CUDA, "wavefront smoothing: a dependency wait timed out");
+    return PSN_OK;
+}
+
+psn_status psn_ctx_set_counting(psn_ctx *ctx, int mode) {
+    if (!ctx || (mode != PSN_COUNT_AUTO && mode != PSN_COUNT_XTILE)) return PSN_ERR_ARG;
+    ctx->count_mode = mode;
     return PSN_OK;
 }
 

@@ -100,6 +100,8 @@ def lib():
         L.psn_triangulate.restype = ctypes.c_int
         L.psn_ctx_set_smoothing.argtypes = [vp, ctypes.c_int, ctypes.c_int32, ctypes.c_int32]
         L.psn_ctx_set_smoothing.restype = ctypes.c_int
+        L.psn_ctx_set_counting.argtypes = [vp, ctypes.c_int]
+        L.psn_ctx_set_counting.restype = ctypes.c_int
         L.psn_smooth_status.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_smooth_status.restype = ctypes.c_int
         L.psn_launch_count.argtypes = [vp]
@@ -111,7 +113,7 @@ def lib():
 EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
             "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
-            "psn_ctx_set_smoothing", "psn_smooth_status"]
+            "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting"]
 
 
 def _ptr(t):
@@ -305,6 +307,10 @@ class PSN:
     def set_smoothing(self, mode: int = 1, iterations_per_launch: int = 0, points_per_tile: int = 0):
         """1 = one launch per iteration (default), 0 = wavefront (temporally blocked)."""
         self._check(self.L.psn_ctx_set_smoothing(self.h, int(mode), int(iterations_per_launch), int(points_per_tile)))
+
+    def set_counting(self, mode: int = 0):
+        """0 = automatic (warp-per-row k_count3 when a row fits a warp), 1 = x-tiled k_count."""
+        self._check(self.L.psn_ctx_set_counting(self.h, int(mode)))
 
     def smooth_status(self, mesh: Mesh, ws: torch.Tensor, stream=None):
         self._check(self.L.psn_smooth_status(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _stream(stream)))

@@ -79,10 +79,18 @@ def _check_volume(a, label_set=None, spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 
     return mesh
 
 
-def test_random_corpus_bit_exact():
+@pytest.mark.parametrize("counting", [0, 1])
+def test_random_corpus_bit_exact(counting):
+    """Both counting kernels (0 = warp-per-row k_count3, 1 = x-tiled k_count) feed the same
+    scan + emission and must reproduce the oracle bit for bit."""
+    p = gu.psn()
     rng = np.random.default_rng(20240126)
-    for a, ls in _corpus(rng, 120):
-        _check_volume(a, ls, spacing=(0.8, 1.0, 1.5), origin=(-3.0, 2.0, 10.0))
+    try:
+        p.set_counting(counting)
+        for a, ls in _corpus(rng, 120):
+            _check_volume(a, ls, spacing=(0.8, 1.0, 1.5), origin=(-3.0, 2.0, 10.0))
+    finally:
+        p.set_counting(0)
 
 
 def test_two_by_two_by_two_exhaustive():

@@ -17,6 +17,7 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active',
         'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active']
 rep = sys.argv[1]
+STALLS = len(sys.argv) > 2
 out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
@@ -26,3 +27,12 @@ for r in rows[2:]:
         if w in hdr:
             i = hdr.index(w)
             print(f'  {w:80s} {r[i]} {units[i]}')
+    if STALLS:
+        st = []
+        for i, h in enumerate(hdr):
+            if h.startswith('smsp__average_warps_issue_stalled_') and h.endswith('_per_issue_active.ratio'):
+                try:
+                    st.append((float(r[i]), h[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]))
+                except ValueError:
+                    pass
+        print('  stalls/issue:', ', '.join(f'{n}={v:.2f}' for v, n in sorted(st, reverse=True)[:10]))
