@@ -210,8 +210,14 @@ cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int th
 }
 
 template <typename T>
-void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st) {
-    if (fast) {   // rows fit one k_count x-tile: per-word point prefixes are row prefixes
+void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st, int emit_mode) {
+    if (fast && ea.W32 <= 32 && emit_mode == 0) {   // band-staged: shared-memory id lookups
+        if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, 2 * sizeof(BandBuf), st>>>(ea);
+        else k_emit_band<T, false><<<(unsigned)blocks, kBandThreads, 2 * sizeof(BandBuf), st>>>(ea);
+    } else if (fast && ea.W32 <= 32 && emit_mode == 1) {   // rows of <= 32 plane words: lane = word, metadata pipelined
+        if (anz) k_emit_row<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
+        else k_emit_row<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
+    } else if (fast) {   // rows fit one k_count x-tile: per-word point prefixes are row prefixes
         if (anz) k_emit_fast<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
         else k_emit_fast<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
     } else {
@@ -433,11 +439,35 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.first_point = (uint32_t)mesh->first_point; ea.first_quad = (uint32_t)mesh->first_quad;
     ea.first_stencil = (uint32_t)mesh->first_stencil;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
+    int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
+    const int emode = getenv("PSN_EMIT_MODE") ? atoi(getenv("PSN_EMIT_MODE")) : 0;
+    if (L.W32 <= 32 && emode == 0) {   // k_emit_band: one resident wave of CTAs looping over bands
+        int occ = 0;
+        const void *fn = eb == 1 ? (anz ? (const void *)k_emit_band<uint8_t, true> : (const void *)k_emit_band<uint8_t, false>)
+                       : eb == 2 ? (anz ? (const void *)k_emit_band<uint16_t, true> : (const void *)k_emit_band<uint16_t, false>)
+                                 : (anz ? (const void *)k_emit_band<uint32_t, true> : (const void *)k_emit_band<uint32_t, false>);
+        static bool attr = false;
+        if (!attr) {
+            for (const void *f : {(const void *)k_emit_band<uint8_t, true>, (const void *)k_emit_band<uint8_t, false>,
+                                  (const void *)k_emit_band<uint16_t, true>, (const void *)k_emit_band<uint16_t, false>,
+                                  (const void *)k_emit_band<uint32_t, true>, (const void *)k_emit_band<uint32_t, false>})
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(BandBuf)));
+            attr = true;
+        }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBandThreads, 2 * sizeof(BandBuf));
+        blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + kBand - 1) / kBand, (int64_t)ctx->sms * std::max(occ, 1)));
+    } else if (L.W32 <= 32) {   // k_emit_row: one resident wave of warps, each pipelining its rows
+        int occ = 0;
+        const void *fn = eb == 1 ? (anz ? (const void *)k_emit_row<uint8_t, true> : (const void *)k_emit_row<uint8_t, false>)
+                       : eb == 2 ? (anz ? (const void *)k_emit_row<uint16_t, true> : (const void *)k_emit_row<uint16_t, false>)
+                                 : (anz ? (const void *)k_emit_row<uint32_t, true> : (const void *)k_emit_row<uint32_t, false>);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
+        blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * std::max(occ, 1)));
+    }
     const bool fast = (L.M - 1) <= (int64_t)(eb == 1 ? count_xt<uint8_t>() : eb == 2 ? count_xt<uint16_t>() : count_xt<uint32_t>());
-    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, fast, blocks, st);
-    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st);
-    else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st);
+    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, fast, blocks, st, emode);
+    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st, emode);
+    else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st, emode);
     ++ctx->launches;
     return cuda_check(ctx, "emit launch");
 }
