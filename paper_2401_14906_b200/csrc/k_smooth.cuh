@@ -172,6 +172,64 @@ __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
     }
 }
 
+// One Jacobi step on STRUCTURE-OF-ARRAYS offsets (x[W] | y[W] | z[W], stride
+// `ws` floats): one point per thread, so every gather instruction of a warp
+// reads consecutive floats of one array (the AoS float3 layout needs three
+// sector-straddling scalar loads per gather).  +-x neighbours (w-1, w+1) come
+// from the adjacent lanes; lanes 0 / 31 and the last point load them.  The
+// arithmetic is jacobi_update: bit-identical to k_smooth.
+struct SmoothSoA {
+    const float *src;          // SoA window offsets; NULL = all zero (first iteration)
+    float *dst;                // SoA window offsets (own entries written)
+    float *world;              // if non-NULL: write AoS world coordinates here instead of dst
+    const uint8_t *fmask;
+    const uint4 *nbr;
+    const float *points;
+    uint32_t n_own, halo_lo, ws;
+    float lambda, d;
+    double sp[3], org[3];
+};
+
+__global__ void __launch_bounds__(256) k_smooth_soa(SmoothSoA a) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = a.n_own, ws = a.ws;
+    const float *__restrict__ sx = a.src, *__restrict__ sy = a.src + ws, *__restrict__ sz = a.src + 2 * ws;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    // uniform trip count so that every lane takes part in the shuffles
+    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const uint32_t i = base + lane;
+        const bool act = i < n;
+        const uint32_t ii = act ? i : n - 1u;
+        const uint32_t w = a.halo_lo + ii;
+        const uint32_t f = act ? (uint32_t)__ldg(a.fmask + ii) : 0u;
+        const uint4 nb = __ldg(a.nbr + ii);
+        float3 o = make_float3(0.f, 0.f, 0.f), g0 = o, g1 = o, g2 = o, g3 = o;
+        if (a.src) {
+            o = make_float3(__ldg(sx + w), __ldg(sy + w), __ldg(sz + w));
+            g0 = make_float3(__ldg(sx + nb.x), __ldg(sy + nb.x), __ldg(sz + nb.x));
+            g1 = make_float3(__ldg(sx + nb.y), __ldg(sy + nb.y), __ldg(sz + nb.y));
+            g2 = make_float3(__ldg(sx + nb.z), __ldg(sy + nb.z), __ldg(sz + nb.z));
+            g3 = make_float3(__ldg(sx + nb.w), __ldg(sy + nb.w), __ldg(sz + nb.w));
+        }
+        float3 mx, px;
+        mx.x = __shfl_up_sync(kFull, o.x, 1); mx.y = __shfl_up_sync(kFull, o.y, 1); mx.z = __shfl_up_sync(kFull, o.z, 1);
+        px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
+        if (!act) continue;
+        if (a.src && f) {
+            if ((f & 4u) && lane == 0) mx = make_float3(__ldg(sx + w - 1u), __ldg(sy + w - 1u), __ldg(sz + w - 1u));
+            if ((f & 8u) && (lane == 31 || i + 1u >= n)) px = make_float3(__ldg(sx + w + 1u), __ldg(sy + w + 1u), __ldg(sz + w + 1u));
+        }
+        const float3 r = jacobi_update(f, o, mx, px, g0, g1, g2, g3, a.lambda, a.d);
+        if (a.world) {
+            a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
+            a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
+            a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
+        } else {
+            a.dst[w] = r.x; a.dst[ws + w] = r.y; a.dst[2 * ws + w] = r.z;
+        }
+    }
+}
+
 // World coordinates of window entries [w0, w1) from offsets (NULL = anchors).
 __global__ void __launch_bounds__(256) k_finalize(const float *offs, const float *points, float *out,
                                                   int64_t w0, int64_t w1, double sx, double sy, double sz,

@@ -487,6 +487,7 @@ psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, 
 }
 
 namespace {
+int64_t soa_stride(int64_t nw) { return (std::max<int64_t>(nw, 1) + 31) / 32 * 32; }
 struct SmoothLayout { size_t nbr, buf0, buf1, rng, done, sch, total; int64_t nw, U; };
 // [nbr uint4 x P | buf0 float4 x W | buf1 float4 x W | rng int2 x U | done u32 x U | sched]
 SmoothLayout smooth_layout(const psn_mesh *m) {
@@ -495,8 +496,10 @@ SmoothLayout smooth_layout(const psn_mesh *m) {
     L.U = (m->n_points + kTbTileMin - 1) / kTbTileMin;   // schedule arrays sized for the smallest tile
     L.nbr = 0;
     L.buf0 = align_up(16 * (size_t)std::max<int64_t>(m->n_points, 1));
-    L.buf1 = L.buf0 + align_up(16 * (size_t)std::max<int64_t>(L.nw, 1));
-    L.rng = L.buf1 + align_up(16 * (size_t)std::max<int64_t>(L.nw, 1));
+    // offset buffers: float4 [W] (wavefront) or SoA float [3][ws] (per-iteration), ws = W rounded to 32
+    const size_t bufb = std::max<size_t>(16 * (size_t)std::max<int64_t>(L.nw, 1), 12 * (size_t)soa_stride(L.nw));
+    L.buf1 = L.buf0 + align_up(bufb);
+    L.rng = L.buf1 + align_up(bufb);
     L.done = L.rng + align_up(8 * (size_t)std::max<int64_t>(L.U, 1));
     L.sch = L.done + align_up(4 * (size_t)std::max<int64_t>(L.U, 1));
     L.total = L.sch + align_up(sizeof(TbSched));
@@ -585,17 +588,25 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     }
     if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
-        // one launch per Jacobi iteration (float3 buffers in the two buffer slots)
+        // one launch per Jacobi iteration: SoA offset buffers in the two buffer slots
         float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
-        SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
+        SmoothSoA a;
+        memset(&a, 0, sizeof(a));
+        a.fmask = mesh->face_masks; a.nbr = static_cast<const uint4 *>(ws); a.points = mesh->points;
+        a.n_own = (uint32_t)mesh->n_points; a.halo_lo = (uint32_t)mesh->halo_lo_points;
+        a.ws = (uint32_t)soa_stride(SL.nw);
+        a.lambda = relaxation; a.d = constraint_distance;
         for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_smooth_soa, 256, 0);
+        const int64_t gsoa = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
         const float *src = nullptr;
         for (int32_t t = 0; t < iterations; ++t) {
             a.src = src;
             const bool last = (t == iterations - 1);
             a.dst = last ? nullptr : buf[t & 1];
             a.world = last ? out : nullptr;
-            k_smooth<<<(unsigned)gs, 256, 0, st>>>(a);
+            k_smooth_soa<<<(unsigned)gsoa, 256, 0, st>>>(a);
             ++ctx->launches;
             src = a.dst;
         }
