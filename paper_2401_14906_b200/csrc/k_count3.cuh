@@ -40,7 +40,7 @@
 
 namespace psn {
 
-constexpr int kC3Rows = 8;                       // consumer warps = voxel rows per CTA
+constexpr int kC3Rows = 16;                      // voxel rows per CTA (kC3Rows / RPW consumer warps)
 constexpr int kC3MaxStages = 8;                  // ring slots (lattice slices): CountArgs.NS <= this
 constexpr int kC3Threads = 32 * (kC3Rows + 1);   // + one producer warp
 

@@ -33,6 +33,7 @@ struct EmitArgs {
     int64_t cap_points, cap_quads, cap_stencil;
     uint32_t first_point, first_quad, first_stencil;
     ScanHeader *hdr;
+    int probe;                 // experiment: 1 = emit computes everything but stores nothing
 };
 
 __device__ __forceinline__ float anchor_coord(double org, double sp, int64_t idx) {
@@ -627,7 +628,6 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
     BandBuf *buf = reinterpret_cast<BandBuf *>(dsm_band);   // [2]
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
-    __shared__ uint16_t slist[kBandThreads / 32][1024];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     LabelSet ls = a.ls;
     if (!ANZ && sizeof(T) < 4) {
@@ -733,113 +733,162 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
         const int32_t sh_o[3] = {elem_shift(rr0 + rstart[0], 0, 4, 1), elem_shift(rr0 + rstart[1], 0, 4, 1),
                                  elem_shift(rr0 + rstart[2], 0, 4, 1)};
         const int32_t sh_r = elem_shift(rr0, 0, 4, 1);
-        for (int b = warp; b < B; b += kBandThreads / 32) {
-            const int32_t r = rr0 + b;
-            if (r >= R) break;
-            const uint32_t cnt = bb.cnt[sh_r + b];
-            if (cnt == 0) continue;
-            const int32_t j = r % NV, k = kA + r / NV;
-            const bool own = k >= own0 && k < own1;
-            // staged rows: own = range 1 idx b+1; (j-1,k-1) = r0 idx b; (j,k-1) = r0 idx b+1;
-            // (j-1,k) = r1 idx b; (j+1,k) = r1 idx b+2; (j,k+1) = r2 idx b
-            const uint32_t offP = bb.off[1][sh_o[1] + b + 1];
-            const uint32_t qbase = own ? bb.offQ[sh_r + b] : 0u, sbase = own ? bb.offS[sh_r + b] : 0u;
-            if (lane < W32) {   // the row's points by running index: lane = plane word
-                uint32_t mm = bb.m[1][sh_m[1] + (b + 1) * W32 + lane];
-                uint32_t pos = bb.p[1][sh_p[1] + (b + 1) * W32 + lane];
-                while (mm) {
-                    const int bit = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    slist[warp][pos++] = (uint16_t)(lane * 32 + bit);
-                }
-            }
-            __syncwarp();
-            // neighbour row q -> (range, index)
-            const int nq_g[5] = {0, 0, 1, 1, 2};
-            const int nq_i[5] = {b, b + 1, b, b + 2, b};
-            const bool nq_ok[5] = {own && j >= 1 && k >= kA + 1, own && k >= kA + 1, own && j >= 1, own && j + 1 <= N - 2,
-                                   own && k + 1 < kB};
-            uint32_t run_q = 0, run_s = 0;
-            const size_t rowA = ((size_t)(k - (int32_t)a.z_lo) * N + j) * M;
-            const size_t rowB = rowA + M, rowC = rowA + (size_t)N * M, rowD = rowC + M;
-            for (uint32_t base = 0; base < cnt; base += 32) {
-                const uint32_t t = base + lane;
-                const bool act = t < cnt;
-                const int32_t i = act ? slist[warp][t] : 0;
-                const uint32_t wi = offP + t;
-                const uint32_t g = gid_base + wi;
-                uint32_t fm = 0, qb = 0, cA = 0, cA1 = 0, cB = 0, cC = 0;
-                if (act && own) {
-                    const uint32_t A = code_at<T, ANZ>(lab + rowA + i, ls), A1 = code_at<T, ANZ>(lab + rowA + i + 1, ls);
-                    const uint32_t Bv = code_at<T, ANZ>(lab + rowB + i, ls), B1 = code_at<T, ANZ>(lab + rowB + i + 1, ls);
-                    const uint32_t C = code_at<T, ANZ>(lab + rowC + i, ls), C1 = code_at<T, ANZ>(lab + rowC + i + 1, ls);
-                    const uint32_t D = code_at<T, ANZ>(lab + rowD + i, ls), D1 = code_at<T, ANZ>(lab + rowD + i + 1, ls);
-                    const bool XA = A != A1, XB = Bv != B1, XC = C != C1, XD = D != D1;
-                    const bool YAB = A != Bv, YA1 = A1 != B1, YCD = C != D, YC1 = C1 != D1;
-                    const bool ZAC = A != C, ZA1 = A1 != C1, ZBD = Bv != D, ZB1 = B1 != D1;
-                    fm |= ((XA | XB | YAB | YA1) && k >= 1) ? 1u : 0u;          // -z
-                    fm |= ((XA | XC | ZAC | ZA1) && j >= 1) ? 2u : 0u;          // -y
-                    fm |= ((YAB | YCD | ZAC | ZBD) && i >= 1) ? 4u : 0u;        // -x
-                    fm |= ((YA1 | YC1 | ZA1 | ZB1) && i + 3 <= M) ? 8u : 0u;    // +x
-                    fm |= ((XB | XD | ZBD | ZB1) && j + 3 <= N) ? 16u : 0u;     // +y
-                    fm |= ((XC | XD | YCD | YC1) && k + 3 <= (int32_t)a.O) ? 32u : 0u;   // +z
-                    qb |= (XA && j >= 1 && k >= 1) ? 1u : 0u;
-                    qb |= (YAB && i >= 1 && k >= 1) ? 2u : 0u;
-                    qb |= (ZAC && i >= 1 && j >= 1) ? 4u : 0u;
-                    cA = cls_of_code<T, ANZ>(ls, A); cA1 = cls_of_code<T, ANZ>(ls, A1);
-                    cB = cls_of_code<T, ANZ>(ls, Bv); cC = cls_of_code<T, ANZ>(ls, C);
-                }
-                const uint32_t packed = ((uint32_t)__popc(qb) << 16) | (uint32_t)__popc(fm);
-                const uint32_t x = scan3(packed, lane);
-                const uint32_t tot = __shfl_sync(kFull, x, 31);
-                const uint32_t ex = x - packed;
-                if (act) {
-                    a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
-                    a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
-                    a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
-                }
-                if (act && own) {
-                    const uint32_t wl = (uint32_t)i >> 5, below = (1u << (i & 31)) - 1u;
-                    uint32_t gn[5];
+        // The warp's work is a stream of ROUNDS (up to 32 points of one of its rows: rows warp,
+        // warp+8, ...).  Software pipelining: the next round's point selection and its 8 corner-label
+        // loads are issued before the current round is emitted, so a round's gather latency overlaps
+        // the previous round's arithmetic and stores.
+        constexpr int WS = kBandThreads / 32;
+        struct Round {
+            int32_t b, j, k;
+            uint32_t base, cnt, i;
+            bool valid, act, own;
+            uint32_t L[8];   // A, A1, B, B1, C, C1, D, D1 (codes)
+        };
+        int32_t pb = warp, pj = 0, pk = 0;   // prepare cursor: row, its (j, k), next round base
+        uint32_t pbase = 0;
+        {
+            const int32_t r = rr0 + pb;
+            pj = r % NV; pk = kA + r / NV;
+        }
+        auto next_row = [&]() {
+            pb += WS; pj += WS;
+            while (pj >= NV) { pj -= NV; ++pk; }
+            pbase = 0;
+        };
+        auto seek = [&]() {   // skip rows without points
+            while (pb < B && rr0 + pb < R && bb.cnt[sh_r + pb] == 0) next_row();
+        };
+        auto prepare = [&](Round &st) {
+            st.valid = pb < B && rr0 + pb < R;
+            if (!st.valid) return;
+            st.b = pb; st.j = pj; st.k = pk; st.base = pbase;
+            st.cnt = bb.cnt[sh_r + pb];
+            st.own = pk >= own0 && pk < own1;
+            const uint32_t t = pbase + lane;
+            st.act = t < st.cnt;
+            // point t of the row: its word = the last word whose first index <= t (prefixes are
+            // non-decreasing; 5-step binary search over the lanes), then the n-th set bit of it
+            const uint32_t wm_l = lane < W32 ? bb.m[1][sh_m[1] + (pb + 1) * W32 + lane] : 0u;
+            const uint32_t wp_l = lane < W32 ? (uint32_t)bb.p[1][sh_p[1] + (pb + 1) * W32 + lane] : 0xFFFFu;
+            int wsel = 0;
 #pragma unroll
-                    for (int q = 0; q < 5; ++q) {
-                        const int gg = nq_g[q], ii = nq_i[q];
-                        const int e = ii * W32 + (int)wl;
-                        gn[q] = nq_ok[q] ? gid_base + bb.off[gg][sh_o[gg] + ii] + bb.p[gg][e + sh_p[gg]] +
-                                               __popc(bb.m[gg][e + sh_m[gg]] & below)
-                                         : 0u;
-                    }
-                    const uint32_t o = wi - halo_lo;
-                    uint32_t ss = sbase + run_s + (ex & 0xffffu);
-                    a.fmask[o] = (uint8_t)fm;
-                    a.csr_off[o] = a.first_stencil + ss;
-                    if (fm & 1u) a.csr_ids[ss++] = gn[1];      // -z  (j, k-1)
-                    if (fm & 2u) a.csr_ids[ss++] = gn[2];      // -y  (j-1, k)
-                    if (fm & 4u) a.csr_ids[ss++] = g - 1u;     // -x
-                    if (fm & 8u) a.csr_ids[ss++] = g + 1u;     // +x
-                    if (fm & 16u) a.csr_ids[ss++] = gn[3];     // +y  (j+1, k)
-                    if (fm & 32u) a.csr_ids[ss++] = gn[4];     // +z  (j, k+1)
-                    uint32_t qs = qbase + run_q + (ex >> 16);
-                    if (qb & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
-                        *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[0], gn[1], g, gn[2]);
-                        *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cA1);
-                        ++qs;
-                    }
-                    if (qb & 2u) {   // y-quad [(i-1,k-1), (i-1,k), (i,k), (i,k-1)] of row j
-                        *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[1] - 1u, g - 1u, g, gn[1]);
-                        *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cB);
-                        ++qs;
-                    }
-                    if (qb & 4u) {   // z-quad [(i-1,j-1), (i,j-1), (i,j), (i-1,j)] of layer k
-                        *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[2] - 1u, gn[2], g, g - 1u);
-                        *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cC);
-                        ++qs;
-                    }
-                }
-                run_q += tot >> 16;
-                run_s += tot & 0xffffu;
+            for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                const uint32_t pv = __shfl_sync(kFull, wp_l, wsel + s2);
+                if (pv <= t) wsel += s2;
             }
-            __syncwarp();
+            const uint32_t mw = __shfl_sync(kFull, wm_l, wsel), pw = __shfl_sync(kFull, wp_l, wsel);
+            uint32_t nth = t - pw, bitpos = 0;   // position of the nth (0-based) set bit of mw
+#pragma unroll
+            for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                const uint32_t lo = __popc(mw & ((1u << (bitpos + s2)) - 1u) & ~((1u << bitpos) - 1u));
+                if (lo <= nth) { nth -= lo; bitpos += s2; }
+            }
+            st.i = st.act ? (uint32_t)(wsel * 32 + bitpos) : 0u;
+            if (st.act && st.own) {
+                const T *pA = lab + ((size_t)(pk - (int32_t)a.z_lo) * N + pj) * M + st.i;   // rows j, j+1 of slices k, k+1
+                const T *pB = pA + M, *pC = pA + (size_t)N * M, *pD = pC + M;
+                st.L[0] = code_at<T, ANZ>(pA, ls); st.L[1] = code_at<T, ANZ>(pA + 1, ls);
+                st.L[2] = code_at<T, ANZ>(pB, ls); st.L[3] = code_at<T, ANZ>(pB + 1, ls);
+                st.L[4] = code_at<T, ANZ>(pC, ls); st.L[5] = code_at<T, ANZ>(pC + 1, ls);
+                st.L[6] = code_at<T, ANZ>(pD, ls); st.L[7] = code_at<T, ANZ>(pD + 1, ls);
+            }
+            pbase += 32;
+            if (pbase >= st.cnt) { next_row(); seek(); }
+        };
+        // neighbour row q -> (range, index offset from b)
+        const int nq_g[5] = {0, 0, 1, 1, 2};
+        const int nq_d[5] = {0, 1, 0, 2, 0};
+        uint32_t run_q = 0, run_s = 0;
+        seek();
+        Round cur;
+        prepare(cur);
+        while (cur.valid) {
+            Round nxt;
+            prepare(nxt);
+            const int32_t b = cur.b, j = cur.j, k = cur.k;
+            const int32_t i = (int32_t)cur.i;
+            const bool act = cur.act, own = cur.own;
+            if (cur.base == 0) { run_q = 0; run_s = 0; }
+            const uint32_t offP = bb.off[1][sh_o[1] + b + 1];
+            const uint32_t t = cur.base + lane;
+            const uint32_t wi = offP + t;
+            const uint32_t g = gid_base + wi;
+            uint32_t fm = 0, qb = 0, cA = 0, cA1 = 0, cB = 0, cC = 0;
+            if (act && own) {
+                const uint32_t A = cur.L[0], A1 = cur.L[1], Bv = cur.L[2], B1 = cur.L[3];
+                const uint32_t C = cur.L[4], C1 = cur.L[5], D = cur.L[6], D1 = cur.L[7];
+                const bool XA = A != A1, XB = Bv != B1, XC = C != C1, XD = D != D1;
+                const bool YAB = A != Bv, YA1 = A1 != B1, YCD = C != D, YC1 = C1 != D1;
+                const bool ZAC = A != C, ZA1 = A1 != C1, ZBD = Bv != D, ZB1 = B1 != D1;
+                fm |= ((XA | XB | YAB | YA1) && k >= 1) ? 1u : 0u;          // -z
+                fm |= ((XA | XC | ZAC | ZA1) && j >= 1) ? 2u : 0u;          // -y
+                fm |= ((YAB | YCD | ZAC | ZBD) && i >= 1) ? 4u : 0u;        // -x
+                fm |= ((YA1 | YC1 | ZA1 | ZB1) && i + 3 <= M) ? 8u : 0u;    // +x
+                fm |= ((XB | XD | ZBD | ZB1) && j + 3 <= N) ? 16u : 0u;     // +y
+                fm |= ((XC | XD | YCD | YC1) && k + 3 <= (int32_t)a.O) ? 32u : 0u;   // +z
+                qb |= (XA && j >= 1 && k >= 1) ? 1u : 0u;
+                qb |= (YAB && i >= 1 && k >= 1) ? 2u : 0u;
+                qb |= (ZAC && i >= 1 && j >= 1) ? 4u : 0u;
+                cA = cls_of_code<T, ANZ>(ls, A); cA1 = cls_of_code<T, ANZ>(ls, A1);
+                cB = cls_of_code<T, ANZ>(ls, Bv); cC = cls_of_code<T, ANZ>(ls, C);
+            }
+            const uint32_t packed = ((uint32_t)__popc(qb) << 16) | (uint32_t)__popc(fm);
+            const uint32_t x = scan3(packed, lane);
+            const uint32_t tot = __shfl_sync(kFull, x, 31);
+            const uint32_t ex = x - packed;
+            if (a.probe && act) {   // keep the results live without storing them
+                if ((fm ^ qb ^ ex ^ cA ^ cA1 ^ cB ^ cC) == 0x7fffffffu) a.fmask[0] = 1;
+            } else if (act) {
+                a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
+                a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
+                a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
+            }
+            if (act && own && !a.probe) {
+                const uint32_t wl = (uint32_t)i >> 5, below = (1u << (i & 31)) - 1u;
+                // neighbour ids actually referenced by this point's stencil entries / quads
+                const uint32_t need = ((qb & 1u) ? 1u : 0u) | (((fm & 1u) || (qb & 3u)) ? 2u : 0u) |
+                                      (((fm & 2u) || (qb & 5u)) ? 4u : 0u) | ((fm & 16u) ? 8u : 0u) |
+                                      ((fm & 32u) ? 16u : 0u);
+                uint32_t gn[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const int gg = nq_g[q], ii = b + nq_d[q];
+                    const int e = ii * W32 + (int)wl;
+                    gn[q] = ((need >> q) & 1u) ? gid_base + bb.off[gg][sh_o[gg] + ii] + bb.p[gg][e + sh_p[gg]] +
+                                                     __popc(bb.m[gg][e + sh_m[gg]] & below)
+                                               : 0u;
+                }
+                const uint32_t qbase = bb.offQ[sh_r + b], sbase = bb.offS[sh_r + b];
+                const uint32_t o = wi - halo_lo;
+                uint32_t ss = sbase + run_s + (ex & 0xffffu);
+                a.fmask[o] = (uint8_t)fm;
+                a.csr_off[o] = a.first_stencil + ss;
+                if (fm & 1u) a.csr_ids[ss++] = gn[1];      // -z  (j, k-1)
+                if (fm & 2u) a.csr_ids[ss++] = gn[2];      // -y  (j-1, k)
+                if (fm & 4u) a.csr_ids[ss++] = g - 1u;     // -x
+                if (fm & 8u) a.csr_ids[ss++] = g + 1u;     // +x
+                if (fm & 16u) a.csr_ids[ss++] = gn[3];     // +y  (j+1, k)
+                if (fm & 32u) a.csr_ids[ss++] = gn[4];     // +z  (j, k+1)
+                uint32_t qs = qbase + run_q + (ex >> 16);
+                if (qb & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
+                    *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[0], gn[1], g, gn[2]);
+                    *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cA1);
+                    ++qs;
+                }
+                if (qb & 2u) {   // y-quad [(i-1,k-1), (i-1,k), (i,k), (i,k-1)] of row j
+                    *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[1] - 1u, g - 1u, g, gn[1]);
+                    *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cB);
+                    ++qs;
+                }
+                if (qb & 4u) {   // z-quad [(i-1,j-1), (i,j-1), (i,j), (i-1,j)] of layer k
+                    *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[2] - 1u, gn[2], g, g - 1u);
+                    *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cC);
+                    ++qs;
+                }
+            }
+            run_q += tot >> 16;
+            run_s += tot & 0xffffu;
+            cur = nxt;
         }
     }
 }

@@ -350,8 +350,8 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
             const int64_t RB = (int64_t)align16((size_t)(L.M * eb)) + 32;   // row + 32-byte pad (pad_row)
             // ring depth: as many slices as keep 3 CTAs resident per SM (<= ~70 KB each), 3..8
             const int64_t SBy = (int64_t)(kC3Rows + 1) * RB;
-            int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, (70 * 1024) / SBy));
-            if (const char *e = getenv("PSN_COUNT_NS")) ns = std::max(3, std::min(kC3MaxStages, atoi(e)));
+            int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, (108 * 1024) / SBy));
+            if (const char *e = getenv("PSN_COUNT_NS")) ns = std::max(2, std::min(kC3MaxStages, atoi(e)));
             const size_t smem = (size_t)ns * (size_t)(kC3Rows + 1) * (size_t)RB;
             ca.NS = ns;
             ca.nXT = 1; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB; ca.multi_xt = 0;
@@ -439,6 +439,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.first_point = (uint32_t)mesh->first_point; ea.first_quad = (uint32_t)mesh->first_quad;
     ea.first_stencil = (uint32_t)mesh->first_stencil;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
+    ea.probe = getenv("PSN_EMIT_PROBE") ? atoi(getenv("PSN_EMIT_PROBE")) : 0;
     int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
     const int emode = getenv("PSN_EMIT_MODE") ? atoi(getenv("PSN_EMIT_MODE")) : 0;
     if (L.W32 <= 32 && emode == 0) {   // k_emit_band: one resident wave of CTAs looping over bands
