@@ -206,6 +206,16 @@ psn_status psn_ctx_set_smoothing(psn_ctx *ctx, int mode, int32_t iterations_per_
 enum { PSN_COUNT_AUTO = 0, PSN_COUNT_XTILE = 1 };
 psn_status psn_ctx_set_counting(psn_ctx *ctx, int mode);
 
+/* Emission kernel of psn_extract(PSN_EMIT) (Pass 4):
+ *   PSN_EMIT_AUTO (default): band-staged k_emit_band (TMA-staged point planes,
+ *     warp-per-row emission) when a row has <= 32 point-plane words (M <= 1025);
+ *   PSN_EMIT_ROW: k_emit_row (row metadata pipelined one row ahead), same limit;
+ *   PSN_EMIT_SCAN: the general k_emit (per-row packed prefix scans, any width).
+ * Wider rows always use the row-prefix / scan kernels.  All produce identical
+ * outputs (tested). */
+enum { PSN_EMIT_AUTO = 0, PSN_EMIT_ROW = 1, PSN_EMIT_SCAN = 2 };
+psn_status psn_ctx_set_emission(psn_ctx *ctx, int mode);
+
 /* Synchronising check of the last psn_smooth on ws: PSN_ERR_CUDA if a
  * wavefront dependency wait timed out (a guard that must never trigger). */
 psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, void *stream);

@@ -51,7 +51,6 @@ struct CountArgs {
     LabelSet ls;
     int multi_xt;              // several x-tiles per row: accumulate with global atomics
     int tma;                   // rows are 16-byte aligned: stage with cp.async.bulk
-    int probe;                 // k_count3 experiment: 1 = consumers only wait/release (memory pipeline alone)
     int NS;                    // k_count3 ring slots
 };
 

@@ -33,7 +33,6 @@ struct EmitArgs {
     int64_t cap_points, cap_quads, cap_stencil;
     uint32_t first_point, first_quad, first_stencil;
     ScanHeader *hdr;
-    int probe;                 // experiment: 1 = emit computes everything but stores nothing
 };
 
 __device__ __forceinline__ float anchor_coord(double org, double sp, int64_t idx) {
@@ -836,14 +835,12 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
             const uint32_t x = scan3(packed, lane);
             const uint32_t tot = __shfl_sync(kFull, x, 31);
             const uint32_t ex = x - packed;
-            if (a.probe && act) {   // keep the results live without storing them
-                if ((fm ^ qb ^ ex ^ cA ^ cA1 ^ cB ^ cC) == 0x7fffffffu) a.fmask[0] = 1;
-            } else if (act) {
+            if (act) {
                 a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
                 a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
                 a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
             }
-            if (act && own && !a.probe) {
+            if (act && own) {
                 const uint32_t wl = (uint32_t)i >> 5, below = (1u << (i & 31)) - 1u;
                 // neighbour ids actually referenced by this point's stencil entries / quads
                 const uint32_t need = ((qb & 1u) ? 1u : 0u) | (((fm & 1u) || (qb & 3u)) ? 2u : 0u) |

@@ -41,6 +41,7 @@ struct psn_ctx {
     int32_t smooth_group = 0;                 // iterations per wavefront launch (0 = automatic)
     int32_t smooth_tile = 0;                  // points per wavefront tile (0 = automatic)
     int count_mode = PSN_COUNT_AUTO;          // psn_ctx_set_counting
+    int emit_mode = PSN_EMIT_AUTO;            // psn_ctx_set_emission
 };
 
 namespace {
@@ -334,7 +335,6 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
         ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask); ca.ppre = at<uint16_t>(ws, L.ppre);
         ca.ls = ls;
-        ca.probe = 0;
         ca.tma = ((L.M * eb) % 16 == 0) && ((reinterpret_cast<uintptr_t>(slab0) & 15u) == 0);
         cudaError_t ce;
         if (use3) {
@@ -351,7 +351,6 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
             // ring depth: as many slices as keep 3 CTAs resident per SM (<= ~70 KB each), 3..8
             const int64_t SBy = (int64_t)(kC3Rows + 1) * RB;
             int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, (108 * 1024) / SBy));
-            if (const char *e = getenv("PSN_COUNT_NS")) ns = std::max(2, std::min(kC3MaxStages, atoi(e)));
             const size_t smem = (size_t)ns * (size_t)(kC3Rows + 1) * (size_t)RB;
             ca.NS = ns;
             ca.nXT = 1; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB; ca.multi_xt = 0;
@@ -439,9 +438,8 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.first_point = (uint32_t)mesh->first_point; ea.first_quad = (uint32_t)mesh->first_quad;
     ea.first_stencil = (uint32_t)mesh->first_stencil;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
-    ea.probe = getenv("PSN_EMIT_PROBE") ? atoi(getenv("PSN_EMIT_PROBE")) : 0;
     int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
-    const int emode = getenv("PSN_EMIT_MODE") ? atoi(getenv("PSN_EMIT_MODE")) : 0;
+    const int emode = ctx->emit_mode;
     if (L.W32 <= 32 && emode == 0) {   // k_emit_band: one resident wave of CTAs looping over bands
         int occ = 0;
         const void *fn = eb == 1 ? (anz ? (const void *)k_emit_band<uint8_t, true> : (const void *)k_emit_band<uint8_t, false>)
@@ -465,7 +463,8 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
         blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * std::max(occ, 1)));
     }
-    const bool fast = (L.M - 1) <= (int64_t)(eb == 1 ? count_xt<uint8_t>() : eb == 2 ? count_xt<uint16_t>() : count_xt<uint32_t>());
+    const bool fast = emode != PSN_EMIT_SCAN &&
+                      (L.M - 1) <= (int64_t)(eb == 1 ? count_xt<uint8_t>() : eb == 2 ? count_xt<uint16_t>() : count_xt<uint32_t>());
     if (eb == 1) dispatch_emit<uint8_t>(ea, anz, fast, blocks, st, emode);
     else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st, emode);
     else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st, emode);
@@ -660,6 +659,12 @@ psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws,
         cudaStreamSynchronize(st) != cudaSuccess)
         return cuda_check(ctx, "smooth status read-back");
     if (h.error) return fail(ctx, PSN_ERR_CUDA, "wavefront smoothing: a dependency wait timed out");
+    return PSN_OK;
+}
+
+psn_status psn_ctx_set_emission(psn_ctx *ctx, int mode) {
+    if (!ctx || (mode != PSN_EMIT_AUTO && mode != PSN_EMIT_ROW && mode != PSN_EMIT_SCAN)) return PSN_ERR_ARG;
+    ctx->emit_mode = mode;
     return PSN_OK;
 }
 

@@ -100,6 +100,8 @@ def lib():
         L.psn_triangulate.restype = ctypes.c_int
         L.psn_ctx_set_smoothing.argtypes = [vp, ctypes.c_int, ctypes.c_int32, ctypes.c_int32]
         L.psn_ctx_set_smoothing.restype = ctypes.c_int
+        L.psn_ctx_set_emission.argtypes = [vp, ctypes.c_int]
+        L.psn_ctx_set_emission.restype = ctypes.c_int
         L.psn_ctx_set_counting.argtypes = [vp, ctypes.c_int]
         L.psn_ctx_set_counting.restype = ctypes.c_int
         L.psn_smooth_status.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
@@ -113,7 +115,8 @@ def lib():
 EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
             "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
-            "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting"]
+            "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting",
+            "psn_ctx_set_emission"]
 
 
 def _ptr(t):
@@ -311,6 +314,10 @@ class PSN:
     def set_counting(self, mode: int = 0):
         """0 = automatic (warp-per-row k_count3 when a row fits a warp), 1 = x-tiled k_count."""
         self._check(self.L.psn_ctx_set_counting(self.h, int(mode)))
+
+    def set_emission(self, mode: int = 0):
+        """0 = automatic (band-staged k_emit_band), 1 = k_emit_row, 2 = general scan-based k_emit."""
+        self._check(self.L.psn_ctx_set_emission(self.h, int(mode)))
 
     def smooth_status(self, mesh: Mesh, ws: torch.Tensor, stream=None):
         self._check(self.L.psn_smooth_status(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _stream(stream)))

@@ -79,18 +79,20 @@ def _check_volume(a, label_set=None, spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 
     return mesh
 
 
-@pytest.mark.parametrize("counting", [0, 1])
-def test_random_corpus_bit_exact(counting):
-    """Both counting kernels (0 = warp-per-row k_count3, 1 = x-tiled k_count) feed the same
-    scan + emission and must reproduce the oracle bit for bit."""
+@pytest.mark.parametrize("counting,emission", [(0, 0), (1, 0), (0, 1), (0, 2), (1, 2)])
+def test_random_corpus_bit_exact(counting, emission):
+    """Every counting kernel (0 = warp-per-row k_count3, 1 = x-tiled k_count) and emission kernel
+    (0 = band-staged, 1 = row-pipelined, 2 = general scan-based) reproduces the oracle bit for bit."""
     p = gu.psn()
     rng = np.random.default_rng(20240126)
     try:
         p.set_counting(counting)
+        p.set_emission(emission)
         for a, ls in _corpus(rng, 120):
             _check_volume(a, ls, spacing=(0.8, 1.0, 1.5), origin=(-3.0, 2.0, 10.0))
     finally:
         p.set_counting(0)
+        p.set_emission(0)
 
 
 def test_two_by_two_by_two_exhaustive():
@@ -258,3 +260,13 @@ def test_wavefront_smoothing_bit_identical(G, tile):
             assert err.max() <= TOL
     finally:
         p.set_smoothing(1, 0, 0)
+
+
+def test_dense_wide_rows_and_layers_smoothing():
+    """Dense iid volumes whose rows hold ~1400 points and whose layers hold ~600K points, so
+    stencil neighbours are far apart in id space: extraction and smoothing still match the oracle."""
+    rng = np.random.default_rng(123)
+    a = rng.integers(0, 4, size=(4, 6, 1500)).astype(np.uint16)
+    _check_volume(a, T=3)
+    a = rng.integers(0, 4, size=(3, 820, 820)).astype(np.uint8)
+    _check_volume(a, T=2)
