@@ -127,12 +127,13 @@ psn_status psn_extract_workspace(const psn_volume *vol, size_t *bytes);
 
 /*
  * Surface extraction (PAPER sec 2.3, Passes 1-4).
- *   phase & PSN_COUNT: Passes 1-3 -- per voxel row point/quad/stencil counts,
- *       trims and point bit-planes (k_count), then the row-wise exclusive scan
- *       (k_scan).  Reads 3 totals back (one stream synchronisation) into
+ *   phase & PSN_COUNT: Passes 1-3 -- per voxel row point/quad/stencil counts
+ *       and point bit-planes (k_count3, or the x-tiled k_count for wide rows;
+ *       psn_ctx_set_counting), then the row-wise exclusive scan (k_scan).  Reads 3 totals back (one stream synchronisation) into
  *       mesh->n_points/n_quads/n_stencil/halo_*.  PSN_ERR_OVERFLOW if any total
  *       reaches 2^32.
- *   phase == PSN_EMIT: Pass 4 (k_emit) into the caller's arrays, using the
+ *   phase == PSN_EMIT: Pass 4 (k_emit_band / k_emit_row / k_emit_fast / k_emit,
+ *       psn_ctx_set_emission) into the caller's arrays, using the
  *       scan kept in `ws` by the preceding PSN_COUNT.  Capacities are checked on
  *       the host against the counted totals (PSN_ERR_CAPACITY, nothing launched).
  *   phase == PSN_COUNT|PSN_EMIT: fully stream-ordered, no host sync: the emit
