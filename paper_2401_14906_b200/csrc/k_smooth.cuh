@@ -16,6 +16,14 @@
 
 namespace psn {
 
+constexpr uint32_t kNbrIdx = 0x3FFFFFFFu;
+__device__ __forceinline__ uint4 nbr_idx(uint4 v) {
+    return make_uint4(v.x & kNbrIdx, v.y & kNbrIdx, v.z & kNbrIdx, v.w);
+}
+__device__ __forceinline__ uint32_t nbr_faces(uint4 v) {
+    return (v.x >> 30) | ((v.y >> 30) << 2) | ((v.z >> 30) << 4);
+}
+
 struct SmoothArgs {
     const float *src;          // window offsets [n_window][3]; NULL = all zero
     float *dst;                // window offsets (own entries written)
@@ -63,8 +71,7 @@ __device__ __forceinline__ float3 jacobi_update(uint32_t f, float3 o, float3 mx,
     if (!f) return o;
     const int deg = __popc(f);
     const float fd = (float)deg;
-    const float inv = deg == 1 ? 1.f : deg == 2 ? 0.5f : deg == 3 ? (1.f / 3.f) : deg == 4 ? 0.25f
-                    : deg == 5 ? 0.2f : (1.f / 6.f);
+    const float inv = __frcp_rn(fd);   // correctly rounded 1/deg (== the constants 1, 1/2, 1/3, ... 1/6)
     const float ex = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
     const float ey = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
     const float ez = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
@@ -75,7 +82,8 @@ __device__ __forceinline__ float3 jacobi_update(uint32_t f, float3 o, float3 mx,
 
 // Smoothing cache: from the CSR stencil, a fixed-stride table of
 // the -z,-y,+y,+z neighbour WINDOW indices of every own point (slots of absent
-// faces hold the point itself).  The +-x neighbours need no table: ids are
+// faces hold the point itself); bits 30-31 of x, y, z carry the face mask
+// (bits 0-1, 2-3, 4-5), readers mask indices with kNbrIdx.  The +-x neighbours need no table: ids are
 // row-major, so they are w-1 / w+1 (reading Q4).  Built once per psn_smooth.
 __global__ void __launch_bounds__(256) k_smooth_prep(const uint8_t *fmask, const uint32_t *csr_off,
                                                      const uint32_t *csr_ids, uint4 *nbr, int64_t n_own,
@@ -91,6 +99,8 @@ __global__ void __launch_bounds__(256) k_smooth_prep(const uint8_t *fmask, const
         if (f & 8u) ++s;                              // +x  (w + 1)
         if (f & 16u) v.z = csr_ids[s++] - win_base;   // +y
         if (f & 32u) v.w = csr_ids[s++] - win_base;   // +z
+        // the face mask rides in the top two bits of x, y, z (window indices < 2^30, checked on the host)
+        v.x |= (f & 3u) << 30; v.y |= ((f >> 2) & 3u) << 30; v.z |= ((f >> 4) & 3u) << 30;
         nbr[i] = v;
     }
 }
@@ -121,7 +131,7 @@ __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
             const uint32_t ii = i[u] < n ? i[u] : n - 1u;
             w[u] = a.halo_lo + ii;
             f[u] = i[u] < n ? (uint32_t)__ldg(a.fmask + ii) : 0u;
-            nb[u] = __ldg(a.nbr + ii);
+            nb[u] = nbr_idx(__ldg(a.nbr + ii));
             o[u] = src ? ld3(src, w[u]) : make_float3(0.f, 0.f, 0.f);
         }
         // y/z gathers (all issued before the arithmetic)
@@ -201,8 +211,9 @@ __global__ void __launch_bounds__(256) k_smooth_soa(SmoothSoA a) {
         const bool act = i < n;
         const uint32_t ii = act ? i : n - 1u;
         const uint32_t w = a.halo_lo + ii;
-        const uint32_t f = act ? (uint32_t)__ldg(a.fmask + ii) : 0u;
-        const uint4 nb = __ldg(a.nbr + ii);
+        const uint4 nbw = __ldg(a.nbr + ii);
+        const uint32_t f = act ? nbr_faces(nbw) : 0u;
+        const uint4 nb = nbr_idx(nbw);
         float3 o = make_float3(0.f, 0.f, 0.f), g0 = o, g1 = o, g2 = o, g3 = o;
         if (a.src) {
             o = make_float3(__ldg(sx + w), __ldg(sy + w), __ldg(sz + w));

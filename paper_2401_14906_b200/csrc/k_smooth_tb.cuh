@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint4 *nbr, const uin
     uint32_t lo = 0xffffffffu, hi = 0u;
     for (uint32_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
         const uint32_t f = fmask[i];
-        const uint4 v = nbr[i];   // absent faces hold the point itself
+        const uint4 v = nbr_idx(nbr[i]);   // absent faces hold the point itself
         lo = min(lo, min(min(v.x, v.y), min(v.z, v.w)));
         hi = max(hi, max(max(v.x, v.y), max(v.z, v.w)));
         lo = min(lo, i - ((f >> 2) & 1u));
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256, 4) k_smooth_tb(TbArgs a) {
                 i[q] = base + 32u * q + lane;
                 const uint32_t ii = i[q] < p1 ? i[q] : p1 - 1u;
                 f[q] = i[q] < p1 ? (uint32_t)__ldg(a.fmask + ii) : 0u;
-                nbv[q] = __ldg(a.nbr + ii);
+                nbv[q] = nbr_idx(__ldg(a.nbr + ii));
                 o[q] = src ? ldcg4(src + ii) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             float4 gth[2][4];

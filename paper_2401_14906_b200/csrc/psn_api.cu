@@ -516,6 +516,8 @@ psn_status psn_smooth_workspace(const psn_mesh *mesh, size_t *bytes) {
 namespace {
 psn_status check_smooth_args(psn_ctx *ctx, const psn_mesh *mesh, float relaxation, float d) {
     if (!mesh) return fail(ctx, PSN_ERR_ARG, "mesh is NULL");
+    if (mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points >= (1ll << 30))
+        return fail(ctx, PSN_ERR_OVERFLOW, "smoothing supports windows of < 2^30 points");
     if (!(relaxation >= 0.f && relaxation <= 1.f)) return fail(ctx, PSN_ERR_ARG, "relaxation must be in [0,1]");
     if (!(d >= 0.f)) return fail(ctx, PSN_ERR_ARG, "constraint distance must be >= 0");
     if (mesh->n_points < 0 || mesh->halo_lo_points < 0 || mesh->halo_hi_points < 0)
