@@ -608,6 +608,7 @@ __global__ void __launch_bounds__(256) k_emit_row(EmitArgs a) {
 // memory.
 constexpr int kBand = 32;
 constexpr int kBandThreads = 256;
+constexpr uint32_t kStageCsr = 150;   // rounds with >= this many CSR ids write them through shared memory
 
 constexpr int kRangeCap = (kBand + 2) * 32 + 16;   // elements per staged range (+ alignment slack)
 struct BandBuf {                      // one stage; word / prefix ranges keep the workspace's row stride W32
@@ -627,6 +628,7 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
     BandBuf *buf = reinterpret_cast<BandBuf *>(dsm_band);   // [2]
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
+    __shared__ uint32_t scsr[kBandThreads / 32][6 * 32];   // a round's CSR ids, written out coalesced
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     LabelSet ls = a.ls;
     if (!ANZ && sizeof(T) < 4) {
@@ -857,15 +859,18 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
                 }
                 const uint32_t qbase = bb.offQ[sh_r + b], sbase = bb.offS[sh_r + b];
                 const uint32_t o = wi - halo_lo;
-                uint32_t ss = sbase + run_s + (ex & 0xffffu);
                 a.fmask[o] = (uint8_t)fm;
-                a.csr_off[o] = a.first_stencil + ss;
-                if (fm & 1u) a.csr_ids[ss++] = gn[1];      // -z  (j, k-1)
-                if (fm & 2u) a.csr_ids[ss++] = gn[2];      // -y  (j-1, k)
-                if (fm & 4u) a.csr_ids[ss++] = g - 1u;     // -x
-                if (fm & 8u) a.csr_ids[ss++] = g + 1u;     // +x
-                if (fm & 16u) a.csr_ids[ss++] = gn[3];     // +y  (j+1, k)
-                if (fm & 32u) a.csr_ids[ss++] = gn[4];     // +z  (j, k+1)
+                a.csr_off[o] = a.first_stencil + sbase + run_s + (ex & 0xffffu);
+                // dense rounds stage their CSR ids (face order) for a coalesced copy-out below;
+                // sparse rounds store them directly
+                uint32_t *sc = (tot & 0xffffu) >= kStageCsr ? scsr[warp] + (ex & 0xffffu)
+                                                             : a.csr_ids + sbase + run_s + (ex & 0xffffu);
+                if (fm & 1u) *sc++ = gn[1];      // -z  (j, k-1)
+                if (fm & 2u) *sc++ = gn[2];      // -y  (j-1, k)
+                if (fm & 4u) *sc++ = g - 1u;     // -x
+                if (fm & 8u) *sc++ = g + 1u;     // +x
+                if (fm & 16u) *sc++ = gn[3];     // +y  (j+1, k)
+                if (fm & 32u) *sc++ = gn[4];     // +z  (j, k+1)
                 uint32_t qs = qbase + run_q + (ex >> 16);
                 if (qb & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
                     *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[0], gn[1], g, gn[2]);
@@ -882,6 +887,15 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
                     *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cC);
                     ++qs;
                 }
+            }
+            {   // the round's CSR ids are one contiguous range: coalesced copy-out
+                const uint32_t ns = tot & 0xffffu;
+                __syncwarp();
+                if (own && ns >= kStageCsr) {
+                    uint32_t *dst = a.csr_ids + bb.offS[sh_r + b] + run_s;
+                    for (uint32_t e = lane; e < ns; e += 32) dst[e] = scsr[warp][e];
+                }
+                __syncwarp();
             }
             run_q += tot >> 16;
             run_s += tot & 0xffffu;
