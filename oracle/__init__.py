@@ -63,7 +63,7 @@ def _load():
                                        i64, i64, i64, _i64p, _i64p, _i64p]
         lib.oracle_smooth.restype = ctypes.c_int
         lib.oracle_smooth.argtypes = [i64, vp, vp, vp, i64, vp, vp, ctypes.c_int32,
-                                      ctypes.c_double, ctypes.c_double, vp]
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_int, vp]
         lib.oracle_triangulate.restype = ctypes.c_int
         lib.oracle_triangulate.argtypes = [i64, vp, vp, i64, ctypes.c_int, vp]
         _lib = lib
@@ -182,9 +182,13 @@ def extract(vol: Volume, k0: int = 0, k1: int | None = None, point_base: int = 0
     return Mesh(pts, anc, vidx, quads, pairs, off, ids, fm, point_base, stencil_base)
 
 
+BOX, SPHERE = 0, 1
+
+
 def smooth(mesh: Mesh, spacing, iterations: int, relaxation: float, constraint: float,
-           frozen: np.ndarray | None = None) -> np.ndarray:
-    """fp64 Jacobi constrained Laplacian smoothing (Eq. 1); returns float64 [P,3] world coords."""
+           frozen: np.ndarray | None = None, shape: int = BOX) -> np.ndarray:
+    """fp64 Jacobi constrained Laplacian smoothing (Eq. 1); returns float64 [P,3] world coords.
+    shape BOX: |p - anchor|_a <= d*s_a per axis; SPHERE: |p - anchor| <= d*min(s)."""
     lib = _load()
     nP = mesh.n_points
     out = np.zeros((nP, 3), np.float64)
@@ -192,14 +196,18 @@ def smooth(mesh: Mesh, spacing, iterations: int, relaxation: float, constraint: 
     fz = None if frozen is None else np.ascontiguousarray(frozen, np.uint8)
     rc = lib.oracle_smooth(nP, _ptr(np.ascontiguousarray(mesh.anchors)), _ptr(mesh.csr_off),
                            _ptr(mesh.csr_ids), mesh.point_base, _ptr(fz), _ptr(sp),
-                           int(iterations), float(relaxation), float(constraint), _ptr(out))
+                           int(iterations), float(relaxation), float(constraint), int(shape), _ptr(out))
     if rc != 0:
         raise ValueError(f"oracle_smooth: bad arguments rc={rc}")
     return out
 
 
-def triangulate(quads: np.ndarray, points: np.ndarray, id_base: int = 0, strategy: int = 1):
-    """Two triangles per quad; strategy 1 = shortest diagonal (ties -> 0-2), 0 = fixed 0-2."""
+FIXED_02, SHORTEST, MIN_AREA, MOST_COPLANAR = 0, 1, 2, 3
+
+
+def triangulate(quads: np.ndarray, points: np.ndarray, id_base: int = 0, strategy: int = SHORTEST):
+    """Two triangles per quad: 0 = fixed 0-2, 1 = shorter diagonal, 2 = minimum area,
+    3 = most co-planar; ties -> 0-2."""
     lib = _load()
     q = np.ascontiguousarray(quads, np.uint32)
     p = np.ascontiguousarray(points, np.float32)

@@ -20,7 +20,9 @@
  *   - smoothing stencil: face neighbours whose shared face
  *     holds an intersected edge                                P:60, reading Q7
  *   - constrained Laplacian smoothing, Eq. 1, Jacobi           P:64-69, readings Q8-Q12
- *   - triangulation along the shorter diagonal                 P:97, reading Q13
+ *   - constraint box (per axis) or sphere at the voxel centre   P:69, readings Q10, Q26
+ *   - triangulation: fixed, shorter diagonal, minimum area,
+ *     most co-planar                                           P:97, readings Q13, Q27
  *
  * Nothing here is blocked, fused, trimmed, bit-sliced or scanned: every voxel
  * and every lattice edge is visited with the explicit edge lists below, in
@@ -344,7 +346,12 @@ int oracle_extract(const void *labels, int elem_bytes,
  *   for t = 1..T, for every point i with N = deg(i) > 0 and not frozen:
  *       m = (1/N) * sum_{j in stencil(i)} (P^{t-1}_j - P^{t-1}_i)     (Eq. 1, reading Q8)
  *       q = P^{t-1}_i + lambda * m
- *       P^t_i = clamp(q, anchor_i - d*s, anchor_i + d*s) per axis     (readings Q9/Q10)
+ *       shape 0 (box):    P^t_i = clamp(q, anchor_i - d*s, anchor_i + d*s) per axis
+ *                         ("a fraction of the hexahedral voxel cell", readings Q9/Q10)
+ *       shape 1 (sphere): r = d * min(s); if |q - anchor_i| > r then
+ *                         P^t_i = anchor_i + (q - anchor_i) * (r / |q - anchor_i|), else q
+ *                         ("a constraint sphere centered at the voxel center point",
+ *                          reading Q26; the norm is sqrt(dx*dx + dy*dy + dz*dz) in that order)
  *   deg 0 or frozen: P^t_i = P^{t-1}_i.
  * csr_ids are global ids; local index = id - id_base.  `frozen` (may be NULL)
  * marks points held fixed (used only by windowed tests: errors entering from
@@ -353,9 +360,14 @@ int oracle_extract(const void *labels, int elem_bytes,
  */
 int oracle_smooth(int64_t nP, const double *anchors, const uint32_t *csr_off,
                   const uint32_t *csr_ids, int64_t id_base, const uint8_t *frozen,
-                  const double *spacing, int32_t T, double lambda, double d, double *out)
+                  const double *spacing, int32_t T, double lambda, double d, int shape, double *out)
 {
     if (nP < 0 || T < 0 || !(lambda >= 0.0 && lambda <= 1.0) || !(d >= 0.0)) return -1;
+    if (shape != 0 && shape != 1) return -1;
+    double smin = spacing[0];
+    if (spacing[1] < smin) smin = spacing[1];
+    if (spacing[2] < smin) smin = spacing[2];
+    const double r = d * smin;   /* sphere radius, world units */
     double *cur = (double *)malloc((size_t)(nP > 0 ? nP : 1) * 3 * sizeof(double));
     double *nxt = (double *)malloc((size_t)(nP > 0 ? nP : 1) * 3 * sizeof(double));
     if (!cur || !nxt) { free(cur); free(nxt); return -3; }
@@ -369,6 +381,7 @@ int oracle_smooth(int64_t nP, const double *anchors, const uint32_t *csr_off,
                 for (int a = 0; a < 3; ++a) nxt[i * 3 + a] = cur[i * 3 + a];
                 continue;
             }
+            double q[3];
             for (int a = 0; a < 3; ++a) {
                 double sum = 0.0;
                 for (uint32_t n = b; n < e; ++n) {
@@ -376,10 +389,27 @@ int oracle_smooth(int64_t nP, const double *anchors, const uint32_t *csr_off,
                     sum += cur[jdx * 3 + a] - cur[i * 3 + a];
                 }
                 double m = sum / (double)N;
-                double q = cur[i * 3 + a] + lambda * m;
-                double lo = anchors[i * 3 + a] - d * spacing[a];
-                double hi = anchors[i * 3 + a] + d * spacing[a];
-                nxt[i * 3 + a] = q < lo ? lo : (q > hi ? hi : q);
+                q[a] = cur[i * 3 + a] + lambda * m;
+            }
+            if (shape == 0) {
+                for (int a = 0; a < 3; ++a) {
+                    double lo = anchors[i * 3 + a] - d * spacing[a];
+                    double hi = anchors[i * 3 + a] + d * spacing[a];
+                    nxt[i * 3 + a] = q[a] < lo ? lo : (q[a] > hi ? hi : q[a]);
+                }
+            } else {
+                double dx = q[0] - anchors[i * 3 + 0];
+                double dy = q[1] - anchors[i * 3 + 1];
+                double dz = q[2] - anchors[i * 3 + 2];
+                double len = sqrt(dx * dx + dy * dy + dz * dz);
+                if (len > r) {
+                    double f = r / len;
+                    nxt[i * 3 + 0] = anchors[i * 3 + 0] + dx * f;
+                    nxt[i * 3 + 1] = anchors[i * 3 + 1] + dy * f;
+                    nxt[i * 3 + 2] = anchors[i * 3 + 2] + dz * f;
+                } else {
+                    for (int a = 0; a < 3; ++a) nxt[i * 3 + a] = q[a];
+                }
             }
         }
         double *tmp = cur; cur = nxt; nxt = tmp;   /* double buffering */
@@ -390,28 +420,56 @@ int oracle_smooth(int64_t nP, const double *anchors, const uint32_t *csr_off,
 }
 
 /* ------------------------------------------------------------------------ */
-/* Triangulation, shortest diagonal                                   */
+/* Triangulation                                                      */
 /* ------------------------------------------------------------------------ */
 
+/* twice the area of triangle (p, q, r) = |(q - p) x (r - p)|, fp64 from fp32 points
+ * (differences exact; products, differences, sum x+y+z, sqrt correctly rounded) */
+static void tri_normal(const float *p, const float *q, const float *r, double n[3])
+{
+    double u0 = (double)q[0] - (double)p[0], u1 = (double)q[1] - (double)p[1], u2 = (double)q[2] - (double)p[2];
+    double v0 = (double)r[0] - (double)p[0], v1 = (double)r[1] - (double)p[1], v2 = (double)r[2] - (double)p[2];
+    n[0] = u1 * v2 - u2 * v1;
+    n[1] = u2 * v0 - u0 * v2;
+    n[2] = u0 * v1 - u1 * v0;
+}
+
+static double norm3(const double n[3]) { return sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]); }
+
+/* cosine of the angle between the two triangles' normals; 1 if either is degenerate */
+static double coplanarity(const double n[3], const double m[3])
+{
+    double den = norm3(n) * norm3(m);
+    if (den == 0.0) return 1.0;
+    return (n[0] * m[0] + n[1] * m[1] + n[2] * m[2]) / den;
+}
+
 /*
- * Each quad (a,b,c,d) -> two triangles.  Diagonal lengths from the given fp32
- * points, computed in fp64: differences, squares, sum x+y+z in that order
- * (reading Q13 / C-8).  d02^2 <= d13^2 (ties -> 0-2): (a,b,c),(a,c,d);
- * else (a,b,d),(b,c,d).  Triangle 2q and 2q+1 come from quad q.
- * strategy 0 = fixed 0-2 ("greedy", reading Q13), 1 = shortest diagonal.
- * point index = id - id_base.
+ * Each quad (a,b,c,d) -> two triangles: diagonal 0-2 gives (a,b,c),(a,c,d),
+ * diagonal 1-3 gives (a,b,d),(b,c,d); triangles 2q and 2q+1 come from quad q.
+ * Quantities are computed in fp64 from the given fp32 points (reading Q13):
+ *   strategy 0: fixed 0-2 ("greedy", reading Q13)
+ *   strategy 1: shorter diagonal: |c-a|^2 <= |d-b|^2 (differences, squares,
+ *               sum x+y+z)
+ *   strategy 2: minimum area: |n(a,b,c)| + |n(a,c,d)| <= |n(a,b,d)| + |n(b,c,d)|
+ *               (n = cross product, twice the triangle area; reading Q27)
+ *   strategy 3: most co-planar: cos(n(a,b,c), n(a,c,d)) >= cos(n(a,b,d), n(b,c,d))
+ *               (the smaller dihedral deviation; degenerate normals count as
+ *               co-planar; reading Q27)
+ * Ties go to 0-2.  point index = id - id_base.
  */
 int oracle_triangulate(int64_t nQ, const uint32_t *quads, const float *points,
                        int64_t id_base, int strategy, uint32_t *tris)
 {
+    if (strategy < 0 || strategy > 3) return -1;
     for (int64_t q = 0; q < nQ; ++q) {
         const uint32_t *v = quads + q * 4;
         int diag02 = 1;
+        const float *p0 = points + ((int64_t)v[0] - id_base) * 3;
+        const float *p1 = points + ((int64_t)v[1] - id_base) * 3;
+        const float *p2 = points + ((int64_t)v[2] - id_base) * 3;
+        const float *p3 = points + ((int64_t)v[3] - id_base) * 3;
         if (strategy == 1) {
-            const float *p0 = points + ((int64_t)v[0] - id_base) * 3;
-            const float *p1 = points + ((int64_t)v[1] - id_base) * 3;
-            const float *p2 = points + ((int64_t)v[2] - id_base) * 3;
-            const float *p3 = points + ((int64_t)v[3] - id_base) * 3;
             double a0 = (double)p2[0] - (double)p0[0];
             double a1 = (double)p2[1] - (double)p0[1];
             double a2 = (double)p2[2] - (double)p0[2];
@@ -421,7 +479,15 @@ int oracle_triangulate(int64_t nQ, const uint32_t *quads, const float *points,
             double d02 = a0 * a0 + a1 * a1 + a2 * a2;
             double d13 = b0 * b0 + b1 * b1 + b2 * b2;
             diag02 = d02 <= d13;
-        } else if (strategy != 0) return -1;
+        } else if (strategy >= 2) {
+            double n1[3], n2[3], m1[3], m2[3];
+            tri_normal(p0, p1, p2, n1);   /* (a,b,c) */
+            tri_normal(p0, p2, p3, n2);   /* (a,c,d) */
+            tri_normal(p0, p1, p3, m1);   /* (a,b,d) */
+            tri_normal(p1, p2, p3, m2);   /* (b,c,d) */
+            if (strategy == 2) diag02 = norm3(n1) + norm3(n2) <= norm3(m1) + norm3(m2);
+            else diag02 = coplanarity(n1, n2) >= coplanarity(m1, m2);
+        }
         uint32_t *t = tris + q * 6;
         if (diag02) { t[0] = v[0]; t[1] = v[1]; t[2] = v[2]; t[3] = v[0]; t[4] = v[2]; t[5] = v[3]; }
         else        { t[0] = v[0]; t[1] = v[1]; t[2] = v[3]; t[3] = v[1]; t[4] = v[2]; t[5] = v[3]; }

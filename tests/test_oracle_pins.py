@@ -416,6 +416,67 @@ def test_smoothing_planar_interface_fixed():
     assert np.all(out[:, 1] == m.anchors[:, 1])
 
 
+@pytest.mark.parametrize("lam", [0.5, 1.0])
+@pytest.mark.parametrize("sp", [(1.0, 1.0, 1.0), (0.8, 0.8, 1.5)])
+def test_smoothing_sphere_dual_cube_closed_form(lam, sp):
+    """Sphere constraint ("a constraint sphere centered at the voxel center point"; reading
+    Q26: radius r = d*min(s)).  For the dual cube every point moves along its voxel diagonal, whose
+    world direction is s (up to signs), by (0.5 - h_t)|s| with h_t = 0.5 (1 - 2 lambda/3)^t; the
+    sphere binds once that exceeds r and then holds the point at distance r on the same diagonal
+    (the next update points the same way).  So, per axis, offset = max(h_t, 0.5 - r/|s|) in
+    voxel units for every t (derived by hand from Eq. 1)."""
+    a = np.zeros((3, 3, 3), np.uint8)
+    a[1, 1, 1] = 1
+    m = extract(a, spacing=sp)
+    d = 0.5
+    r = d * min(sp)
+    s = np.array(sp)
+    centre = np.array([1.0, 1.0, 1.0]) * s
+    bound = 0.5 - r / np.linalg.norm(s)
+    for T in (1, 2, 3, 4, 10, 25):
+        out = oracle.smooth(m, sp, T, lam, d, shape=oracle.SPHERE)
+        h = max(0.5 * (1 - 2 * lam / 3) ** T, bound)
+        exp = centre + np.sign(m.anchors - centre) * h * s
+        assert np.max(np.abs(out - exp)) < 1e-12, (T, np.max(np.abs(out - exp)))
+    # with lambda = 0.5 the sphere is free for t <= 2 and binds from t = 3 on (unit spacing)
+    if sp == (1.0, 1.0, 1.0) and lam == 0.5:
+        assert 0.5 * (2 / 3) ** 2 > bound > 0.5 * (2 / 3) ** 3
+
+
+def test_smoothing_sphere_radial_projection():
+    """S:417 example: a candidate at distance 2r along +x is projected to anchor + (r, 0, 0); a
+    candidate inside the sphere is unchanged."""
+    m = oracle.Mesh(points=np.zeros((2, 3), np.float32),
+                    anchors=np.array([[0.0, 0.0, 0.0], [2.0, 0.0, 0.0]]),
+                    voxel_idx=np.zeros((2, 3), np.int64), quads=np.zeros((0, 4), np.uint32),
+                    pairs=np.zeros((0, 2), np.uint32), csr_off=np.array([0, 1, 2], np.uint32),
+                    csr_ids=np.array([1, 0], np.uint32), face_mask=np.zeros(2, np.uint8))
+    # lambda = 0.5: point 0's candidate is (1, 0, 0) = 2r with d = 0.5 at unit spacing
+    out = oracle.smooth(m, (1.0, 1.0, 1.0), 1, 0.5, 0.5, shape=oracle.SPHERE)
+    np.testing.assert_array_equal(out[0], [0.5, 0.0, 0.0])
+    np.testing.assert_array_equal(out[1], [1.5, 0.0, 0.0])
+    out = oracle.smooth(m, (1.0, 1.0, 1.0), 1, 0.5, 10.0, shape=oracle.SPHERE)   # r = 10: inside
+    np.testing.assert_array_equal(out[0], [1.0, 0.0, 0.0])
+
+
+def test_smoothing_sphere_containment_and_large_radius():
+    """Containment |p - anchor| <= r on iid data (the sphere binds), and with a radius no point can
+    reach the sphere and the box are both inactive: identical trajectories."""
+    rng = np.random.default_rng(9)
+    a = rng.integers(0, 4, size=(14, 15, 16)).astype(np.uint8)
+    sp = (0.8, 1.0, 1.5)
+    m = extract(a, spacing=sp)
+    d = 0.5
+    out = oracle.smooth(m, sp, 10, 0.5, d, shape=oracle.SPHERE)
+    dist = np.linalg.norm(out - m.anchors, axis=1)
+    r = d * min(sp)
+    assert dist.max() <= r * (1 + 1e-12)
+    assert np.isclose(dist, r).mean() > 0.01
+    big_s = oracle.smooth(m, sp, 10, 0.5, 1e6, shape=oracle.SPHERE)
+    big_b = oracle.smooth(m, sp, 10, 0.5, 1e6, shape=oracle.BOX)
+    np.testing.assert_array_equal(big_s, big_b)
+
+
 def test_window_smoothing_matches_full():
     """Windowed oracle (frozen margin layers) reproduces the full oracle on the
     inner layers exactly -- the basis of the full-size sampled parity tests."""
@@ -453,6 +514,42 @@ def test_triangulation_worked(name):
     else:
         assert tris.tolist() == [[0, 1, 3], [1, 2, 3]]
     assert oracle.triangulate(np.array([[0, 1, 2, 3]], np.uint32), pts, strategy=0).tolist() == [[0, 1, 2], [0, 2, 3]]
+
+
+def _diag(pts, strategy):
+    t = oracle.triangulate(np.array([[0, 1, 2, 3]], np.uint32), np.array(pts, np.float32), strategy=strategy)
+    if t.tolist() == [[0, 1, 2], [0, 2, 3]]:
+        return "02"
+    assert t.tolist() == [[0, 1, 3], [1, 2, 3]]
+    return "13"
+
+
+def test_triangulation_strategies_worked():
+    """P:97 names greedy, shortest diagonal, minimum area and most co-planar (reading Q27 for
+    the last two).  Expected diagonals by hand arithmetic:
+    quad A = (0,0,0),(1,0,0),(1,1,1),(0,1,0) (S:473): |d02|^2 = 3 > |d13|^2 = 2 -> shortest 13;
+      n(a,b,c) = (0,-1,1), n(a,c,d) = (-1,0,1): 2*area 0-2 = 2*sqrt2 = 2.83;
+      n(a,b,d) = (0,0,1), n(b,c,d) = (-1,-1,1): 1 + sqrt3 = 2.73 -> min area 13;
+      cos 0-2 = 1/2, cos 1-3 = 1/sqrt3 = 0.577 -> most co-planar 13.
+    quad B = (2,2,2),(-1,0,0),(2,2,1),(1,2,1): |d02|^2 = 1 < 9 -> shortest 02;
+      n(a,b,c) = (2,-3,0), n(a,c,d) = (0,1,0): sqrt13 + 1 = 4.61;
+      n(a,b,d) = (2,-1,-2), n(b,c,d) = (0,-1,2): 3 + sqrt5 = 5.24 -> min area 02;
+      cos 0-2 = -3/sqrt13 = -0.83, cos 1-3 = -3/(3 sqrt5) = -0.45 -> most co-planar 13.
+    Rotating a quad's vertex order by one swaps the roles of the diagonals (same physical
+    diagonal chosen); a planar square and a degenerate quad tie -> 0-2 for every strategy."""
+    A = [[0, 0, 0], [1, 0, 0], [1, 1, 1], [0, 1, 0]]
+    B = [[2, 2, 2], [-1, 0, 0], [2, 2, 1], [1, 2, 1]]
+    assert [_diag(A, s) for s in (0, 1, 2, 3)] == ["02", "13", "13", "13"]
+    assert [_diag(B, s) for s in (0, 1, 2, 3)] == ["02", "02", "02", "13"]
+    flip = {"02": "13", "13": "02"}
+    for q in (A, B):
+        rot = q[3:] + q[:3]
+        for s in (1, 2, 3):
+            assert _diag(rot, s) == flip[_diag(q, s)]
+    square = [[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]]
+    same = [[0.5, 0.5, 0.5]] * 4
+    for s in (0, 1, 2, 3):
+        assert _diag(square, s) == "02" and _diag(same, s) == "02"
 
 
 def test_triangulation_count_and_subcycles():
