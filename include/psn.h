@@ -49,8 +49,10 @@ typedef enum {
 typedef enum { PSN_U8 = 1, PSN_U16 = 2, PSN_U32 = 4 } psn_dtype;
 
 typedef enum {
-    PSN_TRI_FIXED_02 = 0,   /* "greedy": always diagonal 0-2 (reading Q13) */
-    PSN_TRI_SHORTEST = 1    /* shorter diagonal, ties -> 0-2 */
+    PSN_TRI_FIXED_02 = 0,       /* "greedy": always diagonal 0-2 (reading Q13) */
+    PSN_TRI_SHORTEST = 1,       /* shorter diagonal, ties -> 0-2 */
+    PSN_TRI_MIN_AREA = 2,       /* minimum summed triangle area (reading Q27) */
+    PSN_TRI_MOST_COPLANAR = 3   /* most co-planar triangle pair (reading Q27) */
 } psn_tri;
 
 enum { PSN_COUNT = 1, PSN_EMIT = 2 };
@@ -206,6 +208,16 @@ psn_status psn_ctx_set_smoothing(psn_ctx *ctx, int mode, int32_t iterations_per_
  * Both produce identical counts and point planes (tested). */
 enum { PSN_COUNT_AUTO = 0, PSN_COUNT_XTILE = 1 };
 psn_status psn_ctx_set_counting(psn_ctx *ctx, int mode);
+
+/* Constraint on the total motion of a point relative to its voxel centre
+ * used by psn_smooth:
+ *   PSN_CONSTRAINT_BOX (default): |p - anchor|_a <= d * s_a per axis (reading Q10);
+ *   PSN_CONSTRAINT_SPHERE: |p - anchor| <= d * min(s), radial projection after
+ *     the lambda step ("a constraint sphere centered at the voxel center
+ *     point", reading Q26).  psn_smooth_step (slab path) supports the box only
+ *     and returns PSN_ERR_ARG in sphere mode. */
+enum { PSN_CONSTRAINT_BOX = 0, PSN_CONSTRAINT_SPHERE = 1 };
+psn_status psn_ctx_set_constraint(psn_ctx *ctx, int shape);
 
 /* Emission kernel of psn_extract(PSN_EMIT) (Pass 4):
  *   PSN_EMIT_AUTO (default): band-staged k_emit_band (TMA-staged point planes,

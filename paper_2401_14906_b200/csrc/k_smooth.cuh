@@ -16,6 +16,15 @@
 
 namespace psn {
 
+// Constraint on the total motion relative to the anchor (readings Q10 / Q26), in
+// index-space offsets: box |o_a| <= d per axis; sphere |s (.) o| <= r = d * min(s) (world units).
+struct Constraint {
+    float d;             // box half-width, voxel units
+    int sphere;          // 0 = box, 1 = sphere
+    float r, r2;         // sphere radius (world units) and its square
+    float sx, sy, sz;    // spacing (world units per voxel)
+};
+
 constexpr uint32_t kNbrIdx = 0x3FFFFFFFu;
 __device__ __forceinline__ uint4 nbr_idx(uint4 v) {
     return make_uint4(v.x & kNbrIdx, v.y & kNbrIdx, v.z & kNbrIdx, v.w);
@@ -33,7 +42,8 @@ struct SmoothArgs {
     const float *points;       // window anchors (fp32 voxel centres), for the world output
     int64_t n_own;
     uint32_t halo_lo;          // window index of the first own point
-    float lambda, d;
+    float lambda;
+    Constraint cons;
     double sp[3], org[3];
 };
 
@@ -51,9 +61,25 @@ __device__ __forceinline__ float world_of(float p, float o, double org, double s
 // -z,-y,-x,+x,+y,+z), o = own offset, mx/px = -x/+x neighbours, g0..g3 =
 // -z,-y,+y,+z neighbours (values of absent faces are ignored).
 //   s = e + sum_j o_j - deg * o          (e = sum of the face directions)
-//   o' = clamp(o + lambda * s * (1/deg), -d, d)      (readings Q8, Q9, Q10)
+//   o' = constrain(o + lambda * s * (1/deg))           (readings Q8, Q9, Q10, Q26)
 // Explicit _rn intrinsics: no FMA contraction, a fixed summation order.
 __device__ __forceinline__ float jacobi_axis(float e, float o, float mx, float px, float g0, float g1, float g2,
+                                             float g3, uint32_t f, float fd, float inv, float lambda, float d,
+                                             bool box) {
+    float acc = 0.f;
+    if (f & 4u) acc = __fadd_rn(acc, mx);
+    if (f & 8u) acc = __fadd_rn(acc, px);
+    if (f & 1u) acc = __fadd_rn(acc, g0);
+    if (f & 2u) acc = __fadd_rn(acc, g1);
+    if (f & 16u) acc = __fadd_rn(acc, g2);
+    if (f & 32u) acc = __fadd_rn(acc, g3);
+    const float sum = __fadd_rn(__fadd_rn(e, acc), -__fmul_rn(fd, o));
+    const float q = __fadd_rn(o, __fmul_rn(lambda, __fmul_rn(sum, inv)));
+    return box ? fminf(fmaxf(q, -d), d) : q;
+}
+
+// Box-constraint update (the default path; same arithmetic as jacobi_update_t<false>).
+__device__ __forceinline__ float jacobi_axis_box(float e, float o, float mx, float px, float g0, float g1, float g2,
                                              float g3, uint32_t f, float fd, float inv, float lambda, float d) {
     float acc = 0.f;
     if (f & 4u) acc = __fadd_rn(acc, mx);
@@ -66,7 +92,7 @@ __device__ __forceinline__ float jacobi_axis(float e, float o, float mx, float p
     return fminf(fmaxf(__fadd_rn(o, __fmul_rn(lambda, __fmul_rn(sum, inv))), -d), d);
 }
 
-__device__ __forceinline__ float3 jacobi_update(uint32_t f, float3 o, float3 mx, float3 px, float3 g0, float3 g1,
+__device__ __forceinline__ float3 jacobi_update_box(uint32_t f, float3 o, float3 mx, float3 px, float3 g0, float3 g1,
                                                 float3 g2, float3 g3, float lambda, float d) {
     if (!f) return o;
     const int deg = __popc(f);
@@ -75,9 +101,40 @@ __device__ __forceinline__ float3 jacobi_update(uint32_t f, float3 o, float3 mx,
     const float ex = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
     const float ey = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
     const float ez = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
-    return make_float3(jacobi_axis(ex, o.x, mx.x, px.x, g0.x, g1.x, g2.x, g3.x, f, fd, inv, lambda, d),
-                       jacobi_axis(ey, o.y, mx.y, px.y, g0.y, g1.y, g2.y, g3.y, f, fd, inv, lambda, d),
-                       jacobi_axis(ez, o.z, mx.z, px.z, g0.z, g1.z, g2.z, g3.z, f, fd, inv, lambda, d));
+    return make_float3(jacobi_axis_box(ex, o.x, mx.x, px.x, g0.x, g1.x, g2.x, g3.x, f, fd, inv, lambda, d),
+                       jacobi_axis_box(ey, o.y, mx.y, px.y, g0.y, g1.y, g2.y, g3.y, f, fd, inv, lambda, d),
+                       jacobi_axis_box(ez, o.z, mx.z, px.z, g0.z, g1.z, g2.z, g3.z, f, fd, inv, lambda, d));
+}
+
+template <bool SPHERE>
+__device__ __forceinline__ float3 jacobi_update_t(uint32_t f, float3 o, float3 mx, float3 px, float3 g0, float3 g1,
+                                                  float3 g2, float3 g3, float lambda, const Constraint c) {
+    if (!f) return o;
+    const int deg = __popc(f);
+    const float fd = (float)deg;
+    const float inv = __frcp_rn(fd);   // correctly rounded 1/deg (== the constants 1, 1/2, 1/3, ... 1/6)
+    const float ex = (float)((int)((f >> 3) & 1u) - (int)((f >> 2) & 1u));
+    const float ey = (float)((int)((f >> 4) & 1u) - (int)((f >> 1) & 1u));
+    const float ez = (float)((int)((f >> 5) & 1u) - (int)(f & 1u));
+    constexpr bool box = !SPHERE;
+    float3 q = make_float3(jacobi_axis(ex, o.x, mx.x, px.x, g0.x, g1.x, g2.x, g3.x, f, fd, inv, lambda, c.d, box),
+                           jacobi_axis(ey, o.y, mx.y, px.y, g0.y, g1.y, g2.y, g3.y, f, fd, inv, lambda, c.d, box),
+                           jacobi_axis(ez, o.z, mx.z, px.z, g0.z, g1.z, g2.z, g3.z, f, fd, inv, lambda, c.d, box));
+    if (SPHERE) {   // radial projection onto the sphere of radius r about the anchor (reading Q26)
+        const float wx = __fmul_rn(c.sx, q.x), wy = __fmul_rn(c.sy, q.y), wz = __fmul_rn(c.sz, q.z);
+        const float n2 = __fadd_rn(__fadd_rn(__fmul_rn(wx, wx), __fmul_rn(wy, wy)), __fmul_rn(wz, wz));
+        if (n2 > c.r2) {
+            const float k = __fdiv_rn(c.r, __fsqrt_rn(n2));
+            q = make_float3(__fmul_rn(q.x, k), __fmul_rn(q.y, k), __fmul_rn(q.z, k));
+        }
+    }
+    return q;
+}
+
+__device__ __forceinline__ float3 jacobi_update(uint32_t f, float3 o, float3 mx, float3 px, float3 g0, float3 g1,
+                                                float3 g2, float3 g3, float lambda, const Constraint c) {
+    return c.sphere ? jacobi_update_t<true>(f, o, mx, px, g0, g1, g2, g3, lambda, c)
+                    : jacobi_update_t<false>(f, o, mx, px, g0, g1, g2, g3, lambda, c);
 }
 
 // Smoothing cache: from the CSR stencil, a fixed-stride table of
@@ -169,7 +226,7 @@ __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
                 if ((fu & 4u) && lane == 0 && u == 0) mxo[0] = ld3(src, w[u] - 1u);
                 if ((fu & 8u) && (lane == 31 && u == 1 || i[u] + 1u >= n)) pxo[u] = ld3(src, w[u] + 1u);
             }
-            const float3 r = jacobi_update(fu, o[u], mxo[u], pxo[u], g[u][0], g[u][1], g[u][2], g[u][3], a.lambda, a.d);
+            const float3 r = jacobi_update(fu, o[u], mxo[u], pxo[u], g[u][0], g[u][1], g[u][2], g[u][3], a.lambda, a.cons);
             const uint32_t ww = w[u];
             if (a.world) {
                 a.world[3u * ww + 0u] = world_of(__ldg(a.points + 3u * ww + 0u), r.x, a.org[0], a.sp[0]);
@@ -230,7 +287,69 @@ __global__ void __launch_bounds__(256) k_smooth_soa(SmoothSoA a) {
             if ((f & 4u) && lane == 0) mx = make_float3(__ldg(sx + w - 1u), __ldg(sy + w - 1u), __ldg(sz + w - 1u));
             if ((f & 8u) && (lane == 31 || i + 1u >= n)) px = make_float3(__ldg(sx + w + 1u), __ldg(sy + w + 1u), __ldg(sz + w + 1u));
         }
-        const float3 r = jacobi_update(f, o, mx, px, g0, g1, g2, g3, a.lambda, a.d);
+        const float3 r = jacobi_update_box(f, o, mx, px, g0, g1, g2, g3, a.lambda, a.d);
+        if (a.world) {
+            a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
+            a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
+            a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
+        } else {
+            a.dst[w] = r.x; a.dst[ws + w] = r.y; a.dst[2 * ws + w] = r.z;
+        }
+    }
+}
+
+// Same step with the sphere constraint (separate kernel: the box kernel stays minimal).
+struct SmoothSoASphere {   // k_smooth_soa_sphere: as SmoothSoA plus the sphere (reading Q26)
+    const float *src;          // SoA window offsets; NULL = all zero (first iteration)
+    float *dst;                // SoA window offsets (own entries written)
+    float *world;              // if non-NULL: write AoS world coordinates here instead of dst
+    const uint8_t *fmask;
+    const uint4 *nbr;
+    const float *points;
+    uint32_t n_own, halo_lo, ws;
+    float lambda;
+    Constraint cons;
+    double sp[3], org[3];
+};
+
+__global__ void __launch_bounds__(256) k_smooth_soa_sphere(SmoothSoASphere a) {
+    constexpr bool SPHERE = true;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = a.n_own, ws = a.ws;
+    const float *__restrict__ sx = a.src, *__restrict__ sy = a.src + ws, *__restrict__ sz = a.src + 2 * ws;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    Constraint cons;   // register copy (box: only d is live)
+    cons.d = a.cons.d;
+    cons.sphere = SPHERE;
+    if (SPHERE) { cons.r = a.cons.r; cons.r2 = a.cons.r2; cons.sx = a.cons.sx; cons.sy = a.cons.sy; cons.sz = a.cons.sz; }
+    else { cons.r = cons.r2 = cons.sx = cons.sy = cons.sz = 0.f; }
+    const float lambda = a.lambda;
+    // uniform trip count so that every lane takes part in the shuffles
+    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const uint32_t i = base + lane;
+        const bool act = i < n;
+        const uint32_t ii = act ? i : n - 1u;
+        const uint32_t w = a.halo_lo + ii;
+        const uint4 nbw = __ldg(a.nbr + ii);
+        const uint32_t f = act ? nbr_faces(nbw) : 0u;
+        const uint4 nb = nbr_idx(nbw);
+        float3 o = make_float3(0.f, 0.f, 0.f), g0 = o, g1 = o, g2 = o, g3 = o;
+        if (a.src) {
+            o = make_float3(__ldg(sx + w), __ldg(sy + w), __ldg(sz + w));
+            g0 = make_float3(__ldg(sx + nb.x), __ldg(sy + nb.x), __ldg(sz + nb.x));
+            g1 = make_float3(__ldg(sx + nb.y), __ldg(sy + nb.y), __ldg(sz + nb.y));
+            g2 = make_float3(__ldg(sx + nb.z), __ldg(sy + nb.z), __ldg(sz + nb.z));
+            g3 = make_float3(__ldg(sx + nb.w), __ldg(sy + nb.w), __ldg(sz + nb.w));
+        }
+        float3 mx, px;
+        mx.x = __shfl_up_sync(kFull, o.x, 1); mx.y = __shfl_up_sync(kFull, o.y, 1); mx.z = __shfl_up_sync(kFull, o.z, 1);
+        px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
+        if (!act) continue;
+        if (a.src && f) {
+            if ((f & 4u) && lane == 0) mx = make_float3(__ldg(sx + w - 1u), __ldg(sy + w - 1u), __ldg(sz + w - 1u));
+            if ((f & 8u) && (lane == 31 || i + 1u >= n)) px = make_float3(__ldg(sx + w + 1u), __ldg(sy + w + 1u), __ldg(sz + w + 1u));
+        }
+        const float3 r = jacobi_update_t<true>(f, o, mx, px, g0, g1, g2, g3, lambda, cons);
         if (a.world) {
             a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
             a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
@@ -254,23 +373,53 @@ __global__ void __launch_bounds__(256) k_finalize(const float *offs, const float
     }
 }
 
-// Triangulation: quad q -> tris 2q, 2q+1 (reading Q13 / C-8: diagonals from the
-// fp32 points in fp64, differences, squares, sum x+y+z; ties -> 0-2).
+// Triangulation: quad q -> tris 2q, 2q+1; diagonal 0-2 -> (a,b,c),(a,c,d), 1-3 ->
+// (a,b,d),(b,c,d).  Every quantity in fp64 from the fp32 points with explicit _rn operations
+// in the oracle's order (C-8), so the choice is bit-identical to the host's:
+//   1 shortest diagonal: |c-a|^2 <= |d-b|^2 (differences, squares, x+y+z; reading Q13)
+//   2 minimum area:      |n(a,b,c)| + |n(a,c,d)| <= |n(a,b,d)| + |n(b,c,d)|      (reading Q27)
+//   3 most co-planar:    cos(n(a,b,c), n(a,c,d)) >= cos(n(a,b,d), n(b,c,d))      (reading Q27)
+// with n = cross product; ties -> 0-2; 0 = fixed 0-2 ("greedy").
+struct D3 { double x, y, z; };
+__device__ __forceinline__ D3 tri_normal(const float *p, const float *q, const float *r) {
+    const double u0 = __dsub_rn((double)q[0], (double)p[0]), u1 = __dsub_rn((double)q[1], (double)p[1]),
+                 u2 = __dsub_rn((double)q[2], (double)p[2]);
+    const double v0 = __dsub_rn((double)r[0], (double)p[0]), v1 = __dsub_rn((double)r[1], (double)p[1]),
+                 v2 = __dsub_rn((double)r[2], (double)p[2]);
+    return D3{__dsub_rn(__dmul_rn(u1, v2), __dmul_rn(u2, v1)), __dsub_rn(__dmul_rn(u2, v0), __dmul_rn(u0, v2)),
+              __dsub_rn(__dmul_rn(u0, v1), __dmul_rn(u1, v0))};
+}
+__device__ __forceinline__ double norm3(D3 n) {
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(n.x, n.x), __dmul_rn(n.y, n.y)), __dmul_rn(n.z, n.z)));
+}
+__device__ __forceinline__ double coplanarity(D3 n, D3 m) {
+    const double den = __dmul_rn(norm3(n), norm3(m));
+    if (den == 0.0) return 1.0;
+    return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(n.x, m.x), __dmul_rn(n.y, m.y)), __dmul_rn(n.z, m.z)), den);
+}
+
 __global__ void __launch_bounds__(256) k_triangulate(const uint32_t *quads, const float *points, uint32_t *tris,
-                                                     int64_t nQ, uint32_t win_base, int shortest) {
+                                                     int64_t nQ, uint32_t win_base, int strategy) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nQ; q += (int64_t)gridDim.x * blockDim.x) {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(quads) + q);
         bool d02 = true;
-        if (shortest) {
+        if (strategy != 0) {
             const float *p0 = points + 3 * (int64_t)(v.x - win_base), *p1 = points + 3 * (int64_t)(v.y - win_base);
             const float *p2 = points + 3 * (int64_t)(v.z - win_base), *p3 = points + 3 * (int64_t)(v.w - win_base);
-            double a0 = __dsub_rn((double)p2[0], (double)p0[0]), a1 = __dsub_rn((double)p2[1], (double)p0[1]);
-            double a2 = __dsub_rn((double)p2[2], (double)p0[2]);
-            double b0 = __dsub_rn((double)p3[0], (double)p1[0]), b1 = __dsub_rn((double)p3[1], (double)p1[1]);
-            double b2 = __dsub_rn((double)p3[2], (double)p1[2]);
-            const double da = __dadd_rn(__dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)), __dmul_rn(a2, a2));
-            const double db = __dadd_rn(__dadd_rn(__dmul_rn(b0, b0), __dmul_rn(b1, b1)), __dmul_rn(b2, b2));
-            d02 = da <= db;
+            if (strategy == 1) {
+                double a0 = __dsub_rn((double)p2[0], (double)p0[0]), a1 = __dsub_rn((double)p2[1], (double)p0[1]);
+                double a2 = __dsub_rn((double)p2[2], (double)p0[2]);
+                double b0 = __dsub_rn((double)p3[0], (double)p1[0]), b1 = __dsub_rn((double)p3[1], (double)p1[1]);
+                double b2 = __dsub_rn((double)p3[2], (double)p1[2]);
+                const double da = __dadd_rn(__dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)), __dmul_rn(a2, a2));
+                const double db = __dadd_rn(__dadd_rn(__dmul_rn(b0, b0), __dmul_rn(b1, b1)), __dmul_rn(b2, b2));
+                d02 = da <= db;
+            } else {
+                const D3 n1 = tri_normal(p0, p1, p2), n2 = tri_normal(p0, p2, p3);
+                const D3 m1 = tri_normal(p0, p1, p3), m2 = tri_normal(p1, p2, p3);
+                if (strategy == 2) d02 = __dadd_rn(norm3(n1), norm3(n2)) <= __dadd_rn(norm3(m1), norm3(m2));
+                else d02 = coplanarity(n1, n2) >= coplanarity(m1, m2);
+            }
         }
         uint2 *t = reinterpret_cast<uint2 *>(tris + 6 * q);
         if (d02) { t[0] = make_uint2(v.x, v.y); t[1] = make_uint2(v.z, v.x); t[2] = make_uint2(v.z, v.w); }

@@ -79,7 +79,8 @@ struct TbArgs {
     TbSched *sch;
     uint32_t n, U, tile;
     int32_t t0, G, T;          // this launch runs iterations [t0, t0 + G) of T
-    float lambda, d;
+    float lambda;
+    Constraint cons;
     double sp[3], org[3];
 };
 
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(256, 4) k_smooth_tb(TbArgs a) {
                                                  make_float3(gth[q][0].x, gth[q][0].y, gth[q][0].z),
                                                  make_float3(gth[q][1].x, gth[q][1].y, gth[q][1].z),
                                                  make_float3(gth[q][2].x, gth[q][2].y, gth[q][2].z),
-                                                 make_float3(gth[q][3].x, gth[q][3].y, gth[q][3].z), a.lambda, a.d);
+                                                 make_float3(gth[q][3].x, gth[q][3].y, gth[q][3].z), a.lambda, a.cons);
                 const uint32_t w = i[q];
                 if (last) {
                     a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), res.x, a.org[0], a.sp[0]);

@@ -42,9 +42,12 @@ struct psn_ctx {
     int32_t smooth_tile = 0;                  // points per wavefront tile (0 = automatic)
     int count_mode = PSN_COUNT_AUTO;          // psn_ctx_set_counting
     int emit_mode = PSN_EMIT_AUTO;            // psn_ctx_set_emission
+    int constraint = PSN_CONSTRAINT_BOX;      // psn_ctx_set_constraint
 };
 
 namespace {
+
+float __fmul_rn_host(float r) { volatile float x = r; return x * x; }   // one IEEE fp32 rounding
 
 psn_status fail(psn_ctx *ctx, psn_status s, const char *fmt, ...) {
     if (ctx) {
@@ -527,6 +530,18 @@ psn_status check_smooth_args(psn_ctx *ctx, const psn_mesh *mesh, float relaxatio
     return PSN_OK;
 }
 
+// Box constraint of half-width d (voxel units), or the sphere of radius d*min(s) (reading Q26).
+Constraint make_constraint(int shape, float d, const double *sp) {
+    Constraint c;
+    c.d = d;
+    c.sphere = shape == PSN_CONSTRAINT_SPHERE ? 1 : 0;
+    c.sx = sp ? (float)sp[0] : 1.f; c.sy = sp ? (float)sp[1] : 1.f; c.sz = sp ? (float)sp[2] : 1.f;
+    const double smin = sp ? std::min(sp[0], std::min(sp[1], sp[2])) : 1.0;
+    c.r = (float)((double)d * smin);
+    c.r2 = __fmul_rn_host(c.r);
+    return c;
+}
+
 SmoothArgs smooth_args(const psn_mesh *mesh, const void *ws, float lambda, float d) {
     SmoothArgs a;
     memset(&a, 0, sizeof(a));
@@ -534,7 +549,7 @@ SmoothArgs smooth_args(const psn_mesh *mesh, const void *ws, float lambda, float
     a.nbr = static_cast<const uint4 *>(ws);
     a.points = mesh->points; a.n_own = mesh->n_points;
     a.halo_lo = (uint32_t)mesh->halo_lo_points;
-    a.lambda = lambda; a.d = d;
+    a.lambda = lambda; a.cons = make_constraint(PSN_CONSTRAINT_BOX, d, nullptr);
     return a;
 }
 
@@ -592,25 +607,37 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
         // one launch per Jacobi iteration: SoA offset buffers in the two buffer slots
         float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
+        const Constraint cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
         SmoothSoA a;
+        SmoothSoASphere b;
         memset(&a, 0, sizeof(a));
+        memset(&b, 0, sizeof(b));
         a.fmask = mesh->face_masks; a.nbr = static_cast<const uint4 *>(ws); a.points = mesh->points;
         a.n_own = (uint32_t)mesh->n_points; a.halo_lo = (uint32_t)mesh->halo_lo_points;
         a.ws = (uint32_t)soa_stride(SL.nw);
         a.lambda = relaxation; a.d = constraint_distance;
         for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
+        b.fmask = a.fmask; b.nbr = a.nbr; b.points = a.points; b.n_own = a.n_own; b.halo_lo = a.halo_lo; b.ws = a.ws;
+        b.lambda = relaxation; b.cons = cons;
+        for (int c = 0; c < 3; ++c) { b.sp[c] = a.sp[c]; b.org[c] = a.org[c]; }
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_smooth_soa, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cons.sphere ? (const void *)k_smooth_soa_sphere
+                                                                        : (const void *)k_smooth_soa, 256, 0);
         const int64_t gsoa = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
         const float *src = nullptr;
         for (int32_t t = 0; t < iterations; ++t) {
-            a.src = src;
             const bool last = (t == iterations - 1);
-            a.dst = last ? nullptr : buf[t & 1];
-            a.world = last ? out : nullptr;
-            k_smooth_soa<<<(unsigned)gsoa, 256, 0, st>>>(a);
+            float *dst = last ? nullptr : buf[t & 1];
+            float *world = last ? out : nullptr;
+            if (cons.sphere) {
+                b.src = src; b.dst = dst; b.world = world;
+                k_smooth_soa_sphere<<<(unsigned)gsoa, 256, 0, st>>>(b);
+            } else {
+                a.src = src; a.dst = dst; a.world = world;
+                k_smooth_soa<<<(unsigned)gsoa, 256, 0, st>>>(a);
+            }
             ++ctx->launches;
-            src = a.dst;
+            src = dst;
         }
         return cuda_check(ctx, "smooth launch");
     }
@@ -639,7 +666,7 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     ta.world = out; ta.fmask = mesh->face_masks; ta.nbr = static_cast<const uint4 *>(ws); ta.points = mesh->points;
     ta.rng = rng; ta.done = done; ta.sch = sch;
     ta.n = (uint32_t)nw; ta.U = (uint32_t)U; ta.tile = tile; ta.T = iterations;
-    ta.lambda = relaxation; ta.d = constraint_distance;
+    ta.lambda = relaxation; ta.cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
     for (int c = 0; c < 3; ++c) { ta.sp[c] = vol->spacing[c]; ta.org[c] = vol->origin[c]; }
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * 4, U * iterations));
     for (int32_t t0 = 0; t0 < iterations; t0 += G) {
@@ -661,6 +688,12 @@ psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws,
         cudaStreamSynchronize(st) != cudaSuccess)
         return cuda_check(ctx, "smooth status read-back");
     if (h.error) return fail(ctx, PSN_ERR_CUDA, "wavefront smoothing: a dependency wait timed out");
+    return PSN_OK;
+}
+
+psn_status psn_ctx_set_constraint(psn_ctx *ctx, int shape) {
+    if (!ctx || (shape != PSN_CONSTRAINT_BOX && shape != PSN_CONSTRAINT_SPHERE)) return PSN_ERR_ARG;
+    ctx->constraint = shape;
     return PSN_OK;
 }
 
@@ -693,6 +726,8 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, s
     psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
     if (s != PSN_OK) return s;
     if (!dst) return fail(ctx, PSN_ERR_ARG, "dst is NULL");
+    if (ctx->constraint != PSN_CONSTRAINT_BOX)
+        return fail(ctx, PSN_ERR_ARG, "psn_smooth_step supports the box constraint (the sphere needs psn_smooth)");
     if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
     if (mesh->n_points == 0) return PSN_OK;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
@@ -726,14 +761,14 @@ psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *poin
     ctx->launches = 0;
     if (!mesh || !tris || (mesh->n_quads > 0 && (!mesh->quads || !points)))
         return fail(ctx, PSN_ERR_ARG, "NULL argument");
-    if (tri != PSN_TRI_FIXED_02 && tri != PSN_TRI_SHORTEST) return fail(ctx, PSN_ERR_ARG, "unknown triangulation");
+    if (tri < PSN_TRI_FIXED_02 || tri > PSN_TRI_MOST_COPLANAR) return fail(ctx, PSN_ERR_ARG, "unknown triangulation");
     if ((reinterpret_cast<uintptr_t>(mesh->quads) & 15u) || (reinterpret_cast<uintptr_t>(tris) & 7u))
         return fail(ctx, PSN_ERR_ARG, "quads must be 16-byte and tris 8-byte aligned");
     if (mesh->n_quads == 0) return PSN_OK;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     k_triangulate<<<(unsigned)grid_for(ctx, mesh->n_quads), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         mesh->quads, points, tris, mesh->n_quads, (uint32_t)(mesh->first_point - mesh->halo_lo_points),
-        tri == PSN_TRI_SHORTEST ? 1 : 0);
+        (int)tri);
     ++ctx->launches;
     return cuda_check(ctx, "triangulate launch");
 }

@@ -17,11 +17,12 @@ from dataclasses import dataclass, field
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsn.so")
+LIB_PATH = os.environ.get("PSN_LIB") or os.path.join(_HERE, "libpsn.so")   # PSN_LIB: A/B builds (tools)
 
 PSN_OK, PSN_ERR_ARG, PSN_ERR_LABELS, PSN_ERR_OVERFLOW, PSN_ERR_CAPACITY, PSN_ERR_STATE, PSN_ERR_CUDA = range(7)
 PSN_COUNT, PSN_EMIT = 1, 2
-PSN_TRI_FIXED_02, PSN_TRI_SHORTEST = 0, 1
+PSN_TRI_FIXED_02, PSN_TRI_SHORTEST, PSN_TRI_MIN_AREA, PSN_TRI_MOST_COPLANAR = 0, 1, 2, 3
+PSN_CONSTRAINT_BOX, PSN_CONSTRAINT_SPHERE = 0, 1
 BACKGROUND = 0xFFFFFFFF
 
 _DTYPES = {torch.uint8: 1, torch.uint16: 2, torch.uint32: 4}
@@ -100,6 +101,9 @@ def lib():
         L.psn_triangulate.restype = ctypes.c_int
         L.psn_ctx_set_smoothing.argtypes = [vp, ctypes.c_int, ctypes.c_int32, ctypes.c_int32]
         L.psn_ctx_set_smoothing.restype = ctypes.c_int
+        if hasattr(L, "psn_ctx_set_constraint"):   # (absent from older builds loaded via PSN_LIB)
+            L.psn_ctx_set_constraint.argtypes = [vp, ctypes.c_int]
+            L.psn_ctx_set_constraint.restype = ctypes.c_int
         L.psn_ctx_set_emission.argtypes = [vp, ctypes.c_int]
         L.psn_ctx_set_emission.restype = ctypes.c_int
         L.psn_ctx_set_counting.argtypes = [vp, ctypes.c_int]
@@ -116,7 +120,7 @@ EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_s
             "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
             "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting",
-            "psn_ctx_set_emission"]
+            "psn_ctx_set_emission", "psn_ctx_set_constraint"]
 
 
 def _ptr(t):
@@ -314,6 +318,10 @@ class PSN:
     def set_counting(self, mode: int = 0):
         """0 = automatic (warp-per-row k_count3 when a row fits a warp), 1 = x-tiled k_count."""
         self._check(self.L.psn_ctx_set_counting(self.h, int(mode)))
+
+    def set_constraint(self, shape: int = PSN_CONSTRAINT_BOX):
+        """Motion constraint of psn_smooth: box (per axis, default) or sphere (radius d*min(s))."""
+        self._check(self.L.psn_ctx_set_constraint(self.h, int(shape)))
 
     def set_emission(self, mode: int = 0):
         """0 = automatic (band-staged k_emit_band), 1 = k_emit_row, 2 = general scan-based k_emit."""

@@ -270,3 +270,54 @@ def test_dense_wide_rows_and_layers_smoothing():
     _check_volume(a, T=3)
     a = rng.integers(0, 4, size=(3, 820, 820)).astype(np.uint8)
     _check_volume(a, T=2)
+
+
+@pytest.mark.parametrize("spacing", [(1.0, 1.0, 1.0), (0.8, 0.8, 1.5)])
+def test_sphere_constraint_smoothing(spacing):
+    """psn_smooth with the sphere constraint (reading Q26) against the fp64 oracle: within
+    1e-4 x spacing, and every point within d*min(s) of its voxel centre (+ fp32 rounding); the
+    per-iteration and wavefront schedules stay bit-identical."""
+    p = gu.psn()
+    rng = np.random.default_rng(61)
+    vols = [rng.integers(0, 4, size=(17, 19, 23)).astype(np.uint8),
+            psn_gen.generate_host(psn_gen.config("c1")),
+            np.pad(np.ones((5, 5, 5), np.uint16), 2)]
+    try:
+        p.set_constraint(1)
+        for a in vols:
+            _, vol, mesh, _ = gu.gpu_extract(a, spacing=spacing, origin=(3.0, -1.0, 0.5))
+            om = oracle.extract(oracle.as_volume(a, spacing, (3.0, -1.0, 0.5)))
+            for T in (1, 4, 12):
+                out = p.smooth(vol, mesh, T, 0.5, 0.5)
+                ref = oracle.smooth(om, spacing, T, 0.5, 0.5, shape=oracle.SPHERE)
+                g = out[:om.n_points].cpu().numpy().astype(np.float64)
+                err = np.abs(g - ref) / np.array(spacing)
+                assert err.max() <= TOL, (T, err.max())
+                r = 0.5 * min(spacing)
+                dist = np.linalg.norm(g - om.anchors, axis=1)
+                assert dist.max() <= r + 4 * np.spacing(np.float32(np.abs(g).max())), dist.max() - r
+            ws = p.smooth_workspace(mesh)
+            ref = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws).clone()
+            p.set_smoothing(0, 3, 256)
+            out = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws)
+            p.smooth_status(mesh, ws)
+            p.set_smoothing(1, 0, 0)
+            np.testing.assert_array_equal(out[:mesh.n_points].cpu().numpy(), ref[:mesh.n_points].cpu().numpy())
+    finally:
+        p.set_constraint(0)
+        p.set_smoothing(1, 0, 0)
+
+
+@pytest.mark.parametrize("strategy", [0, 1, 2, 3])
+def test_triangulation_strategies(strategy):
+    """k_triangulate for fixed / shortest / minimum-area / most-co-planar (reading Q27):
+    bit-exact against the host triangulation of the same fp32 points (C-8 i), on smoothed
+    meshes (non-planar quads) and on the unsmoothed voxel-centre mesh (planar quads: ties)."""
+    rng = np.random.default_rng(71)
+    for a in (rng.integers(0, 3, size=(15, 16, 17)).astype(np.uint16), psn_gen.generate_host(psn_gen.config("c1"))):
+        p, vol, mesh, _ = gu.gpu_extract(a, spacing=(0.8, 1.0, 1.5))
+        om = oracle.extract(oracle.as_volume(a, (0.8, 1.0, 1.5)))
+        for pts in (p.smooth(vol, mesh, 6, 0.5, 0.5), mesh.points):
+            tris = p.triangulate(mesh, pts, strategy=strategy)
+            host = oracle.triangulate(om.quads, pts[:om.n_points].cpu().numpy(), strategy=strategy)
+            np.testing.assert_array_equal(gu.u32(tris, 2 * om.n_quads), host)
