@@ -37,6 +37,7 @@ WORKLOADS = {
     "c4": "c4: 1024^3 u16 atlas-like (200 Voronoi labels in a ball + 300 inclusions); extract + 50 smoothing iterations, z-slab over N GPUs",
     "c5a": "c5a: 512^3 u8 iid {0,1,2,3}; extract + 10 smoothing iterations",
     "c5b": "c5b: 512^3 u8 single sphere r=16; extract + 10 smoothing iterations",
+    "c6": "c6 (NEXT-1): 512^3 u16 Synthetic-like, 128 overlapping spheres (P 5.22 M, Q 5.25 M); extract + 25 smoothing iterations",
 }
 TRIANGULATE = {"c2"}
 

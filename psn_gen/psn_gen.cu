@@ -91,6 +91,7 @@ __host__ __device__ static uint32_t psn_gen_voxel(const psn_gen_spec *s, int64_t
     case PSN_GEN_C1:
     case PSN_GEN_C5B:
     case PSN_GEN_SPHERES:
+    case PSN_GEN_C6:
         for (int n = 0; n < s->n_ell; ++n)
             if (in_sphere(x, y, z, s->ell[n])) lab = s->ell_label[n];
         break;
@@ -203,6 +204,19 @@ extern "C" int psn_gen_config(int kind, uint64_t seed, psn_gen_spec *s)
         return 0;
     case PSN_GEN_C5A:
         s->elem_bytes = 1; s->dims[0] = s->dims[1] = s->dims[2] = 512;
+        return 0;
+    case PSN_GEN_C6:
+        /* PAPER Table 1 "Synthetic" (5.21 M points, 10.55 M triangles): 128 labels as
+         * overlapping spheres in painter's order, radius U[rmin, rmax) calibrated so that the quad
+         * count is ~5.28 M, centres uniform in the volume (spheres may be clipped by its faces) */
+        s->elem_bytes = 2; s->dims[0] = s->dims[1] = s->dims[2] = 512;
+        s->n_ell = 128;
+        for (int n = 0; n < 128; ++n) {
+            double r = unif(&st, 48.0, 84.0);
+            for (int a = 0; a < 3; ++a) s->ell[n][a] = unif(&st, 0.0, 511.0);
+            s->ell[n][3] = s->ell[n][4] = s->ell[n][5] = r;
+            s->ell_label[n] = (uint32_t)(n + 1);
+        }
         return 0;
     case PSN_GEN_C5B:
         s->elem_bytes = 1; s->dims[0] = s->dims[1] = s->dims[2] = 512;

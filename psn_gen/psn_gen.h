@@ -26,7 +26,8 @@ enum {
     PSN_GEN_C4 = 4,       /* 1024^3 u16 atlas: 200-seed Voronoi in a ball + 300 inclusions */
     PSN_GEN_C5A = 5,      /* 512^3 u8 iid {0,1,2,3}                                 */
     PSN_GEN_C5B = 6,      /* 512^3 u8 single sphere r=16 at the centre              */
-    PSN_GEN_SPHERES = 7   /* generic: n random spheres in a box (custom dims, used by tests) */
+    PSN_GEN_SPHERES = 7,  /* generic: n random spheres in a box (custom dims, used by tests) */
+    PSN_GEN_C6 = 8        /* 512^3 u16 "Synthetic"-like: 128 overlapping spheres (NEXT-1)  */
 };
 
 #define PSN_GEN_MAX_SEEDS 256

@@ -28,11 +28,15 @@ def test_recipe_vectors():
     s = psn_gen.config("c4")
     assert s.tries_first == 2
     np.testing.assert_allclose(list(s.seeds[0]), [503.576846159, 404.050420913, 600.799583546], atol=1e-9)
+    s = psn_gen.config("c6")   # NEXT-1 Synthetic-like: 128 spheres, r = U[48, 84), centres U[0, 511)
+    assert s.n_ell == 128 and s.ell_label[0] == 1 and s.ell_label[127] == 128
+    np.testing.assert_allclose(list(s.ell[0]), [228.066311285, 28.791222208, 53.930352079,
+                                                74.633412517, 74.633412517, 74.633412517], atol=1e-9)
     a = psn_gen.generate_host(psn_gen.config("c5a"), 0, 1)
     assert a[0, 0, :16].tolist() == [1, 3, 0, 0, 0, 1, 3, 2, 1, 2, 1, 0, 3, 1, 3, 3]
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c5b"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c5b", "c6"])
 def test_slab_equals_full(name):
     s = psn_gen.config(name)
     full = psn_gen.generate_host(s, 0, min(s.O, 40))

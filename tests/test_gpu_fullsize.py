@@ -1,4 +1,4 @@
-"""Full-size parity at BASELINE.json's configs (c3, c4, c5a, c5b), in the launch
+"""Full-size parity at BASELINE.json's configs (c3, c4, c5a, c5b) and the NEXT-1 config c6, in the launch
 configuration bench.py times (psn.Pipeline: PSN_COUNT|PSN_EMIT with
 preallocated capacities, then psn_smooth).
 
@@ -37,7 +37,7 @@ def layer_counts_parallel(vol, nthreads=8):
     return tuple(np.concatenate([p[i] for p in parts]) for i in range(3))
 
 
-@pytest.fixture(scope="module", params=["c3", "c5b", "c5a", "c4"])
+@pytest.fixture(scope="module", params=["c3", "c5b", "c5a", "c4", "c6"])
 def run(request):
     name = request.param
     spec = psn_gen.config(name)
@@ -103,3 +103,28 @@ def test_sampled_smoothing(run):
     gpu = pipe.out[g0:g0 + n].cpu().numpy().astype(np.float64)
     err = np.abs(gpu - ref[sel]) / np.array(run["sp"])
     assert err.max() <= TOL, err.max()
+
+
+@pytest.mark.parametrize("n", [1, 8, 64])
+def test_c6_label_subsets(n):
+    """NEXT-1: extracting only labels {1..n} of the Synthetic-like c6 volume
+    (general label set: bitset-classified kernels) reproduces the oracle's per-layer counts, and
+    a sampled window bit for bit."""
+    spec = psn_gen.config("c6")
+    p = gu.psn()
+    labels = psn_gen.generate_device(spec)
+    vol = p.volume(labels)
+    ls = list(range(1, n + 1))
+    mesh = p.extract(vol, ls)
+    host = labels.cpu().numpy()
+    ovol = oracle.Volume(host, (spec.M, spec.N, spec.O), 0, (1.0, 1.0, 1.0), label_set=tuple(ls))
+    Pl, Ql, Sl = layer_counts_parallel(ovol)
+    assert (mesh.n_points, mesh.n_quads, mesh.n_stencil) == (int(Pl.sum()), int(Ql.sum()), int(Sl.sum()))
+    k0, k1 = 240, 243
+    om = oracle.extract(ovol, k0, k1, point_base=int(Pl[:k0].sum()), stencil_base=int(Sl[:k0].sum()))
+    g = gu.mesh_np(mesh)
+    p0, s0, q0 = int(Pl[:k0].sum()), int(Sl[:k0].sum()), int(Ql[:k0].sum())
+    np.testing.assert_array_equal(g["points"][p0:p0 + om.n_points], om.points)
+    np.testing.assert_array_equal(g["quads"][q0:q0 + om.n_quads], om.quads)
+    np.testing.assert_array_equal(g["pairs"][q0:q0 + om.n_quads], om.pairs)
+    np.testing.assert_array_equal(g["csr_ids"][s0:s0 + om.n_stencil], om.csr_ids)
