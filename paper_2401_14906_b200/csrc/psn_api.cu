@@ -353,7 +353,9 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
             const int64_t RB = (int64_t)align16((size_t)(L.M * eb)) + 32;   // row + 32-byte pad (pad_row)
             // ring depth: as many slices as keep 3 CTAs resident per SM (<= ~70 KB each), 3..8
             const int64_t SBy = (int64_t)(kC3Rows + 1) * RB;
-            int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, (108 * 1024) / SBy));
+            // (a general label set also keeps its 8 KB classification bitset in shared memory)
+            const int64_t budget = 108 * 1024 - ((!anz && eb < 4) ? 8 * 1024 : 0);
+            int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, budget / SBy));
             const size_t smem = (size_t)ns * (size_t)(kC3Rows + 1) * (size_t)RB;
             ca.NS = ns;
             ca.nXT = 1; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB; ca.multi_xt = 0;
