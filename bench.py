@@ -220,7 +220,7 @@ def run_psn(args, rank, world, local_rank):
 
     import psn_gen
     from paper_2401_14906_b200 import PSN
-    from paper_2401_14906_b200.psn import Pipeline, surface_nets_host
+    from paper_2401_14906_b200.psn import Pipeline, SurfaceNetsStream, surface_nets_host
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -323,21 +323,27 @@ def run_psn(args, rank, world, local_rank):
     if world == 1 and not args.no_e2e:
         host = torch.empty(labels.shape, dtype=labels.dtype, pin_memory=True)
         host.copy_(labels)
-        state = {}
-        surface_nets_host(psn, host, sp, T, lam, d, state=state)
+        sns = SurfaceNetsStream(psn, labels.shape, labels.dtype, sp, T, lam, d)
+        for _ in range(sns.depth):                 # warm-up: sizes every slot
+            sns.result(sns.submit(host))
         torch.cuda.synchronize()
-        ke = max(1, min(K, args.e2e_steps))
+        ke = max(1, args.e2e_steps)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(ke):
-            surface_nets_host(psn, host, sp, T, lam, d, state=state)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        e0.record(sns.s_h2d)                       # before the first upload
+        tickets = [sns.submit(host) for _ in range(ke)]
+        e1.record(sns.s_d2h)                       # after the last readback
+        last = sns.result(tickets[-1])             # host outputs of the last volume are in host memory
+        e1.synchronize()
         te = e0.elapsed_time(e1) / ke
+        pts = last[0]
+        state = {"h2d_bytes": sns.h2d_bytes, "d2h_bytes": sns.d2h_bytes}
         e2e = {"value": V / (te * 1e-3), "unit": "voxel/s", "h2d_bytes_per_step": int(state["h2d_bytes"]),
                "d2h_bytes_per_step": int(state["d2h_bytes"]), "ms_per_step": te, "steps": ke,
-               "api": "paper_2401_14906_b200.psn.surface_nets_host (pinned host labels -> device -> pinned host mesh)"}
+               "api": "paper_2401_14906_b200.psn.SurfaceNetsStream (per step: pinned host labels -> device, extract + "
+                      "smooth, device -> pinned host points/quads/two-tuples; consecutive volumes overlap on "
+                      "copy / compute / readback streams)",
+               "timing": "CUDA events: first upload (copy stream) to last readback (readback stream), / steps"}
+        del pts, last, sns
         del host, state
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
@@ -384,7 +390,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="psn", choices=["psn", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-voxels", type=float, default=96e6, help="oracle sample size for cpu_baseline (~10-30 s)")
     ap.add_argument("--ref-voxels", type=float, default=6e6, help="oracle sample size per reference step")

@@ -442,3 +442,113 @@ def surface_nets_host(psn: PSN, labels_host: torch.Tensor, spacing, iterations: 
     state["h2d_bytes"] = labels_host.numel() * labels_host.element_size()
     state["d2h_bytes"] = P * 12 + Q * 24
     return state["h_points"], state["h_quads"], state["h_pairs"]
+
+
+class SurfaceNetsStream:
+    """Pipelined host-buffer API for a sequence of same-shaped label volumes
+    (e.g. a time series of segmentations, or an atlas re-extracted with new
+    labels).
+
+    submit(labels_host) enqueues, for one pinned host volume:
+      copy stream    : host -> device copy of the labels (after the slot's
+                       previous volume has been processed);
+      compute stream : PSN_COUNT (one host synchronisation for the exact totals,
+                       P:86), PSN_EMIT into the slot's mesh (grown if needed),
+                       psn_smooth;
+      readback stream: device -> pinned host copies of the quads and two-tuples
+                       (as soon as extraction is done, overlapping smoothing) and
+                       of the smoothed points.
+    `depth` slots (device labels, workspaces, mesh, smoothing buffers, pinned
+    host outputs) rotate, so volume s+1's upload overlaps volume s's compute and
+    readback (PCIe is full duplex).  result(ticket) waits for that volume's host
+    outputs; they stay valid until `depth` further submissions.  Every step of
+    the path runs in libpsn.so's kernels; this class only orders copies and
+    launches.
+    """
+
+    def __init__(self, psn: PSN, shape, dtype, spacing, iterations: int, relaxation: float, constraint: float,
+                 origin=(0.0, 0.0, 0.0), label_set=None, depth: int = 2):
+        self.psn, self.shape, self.dtype = psn, tuple(shape), dtype
+        self.spacing, self.origin = tuple(spacing), tuple(origin)
+        self.T, self.lam, self.d = iterations, relaxation, constraint
+        self.labels = psn.labels(label_set)
+        self.depth = depth
+        self.dev = f"cuda:{psn.device}"
+        self.s_h2d, self.s_comp, self.s_d2h = (torch.cuda.Stream(device=self.dev) for _ in range(3))
+        self.slots = [dict(labels=torch.empty(self.shape, dtype=dtype, device=self.dev), ws=None, mesh=None,
+                           sws=None, out=None, host=None, counts=None, ev_h2d=torch.cuda.Event(),
+                           ev_ext=torch.cuda.Event(), ev_comp=torch.cuda.Event(), ev_d2h=torch.cuda.Event(),
+                           used=False) for _ in range(depth)]
+        self.n = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def _ensure(self, sl, c):
+        """Grow the slot's device mesh / smoothing buffers / pinned outputs to the counted totals."""
+        nw = c.halo_lo_points + c.n_points + c.halo_hi_points
+        m = sl["mesh"]
+        if m is not None and m.points.shape[0] >= nw and m.quads.shape[0] >= c.n_quads and \
+                m.stencil_ids.shape[0] >= c.n_stencil and m.stencil_offsets.shape[0] >= c.n_points + 1:
+            return
+        torch.cuda.synchronize(self.dev)              # rare: old buffers may still be read back
+        sl["mesh"] = self.psn.alloc_mesh(nw, c.n_points, c.n_quads, c.n_stencil)
+        sl["out"] = torch.empty((max(nw, 1), 3), dtype=torch.float32, device=self.dev)
+        sl["host"] = dict(points=torch.empty((max(c.n_points, 1), 3), dtype=torch.float32, pin_memory=True),
+                          quads=torch.empty((max(c.n_quads, 1), 4), dtype=torch.int32, pin_memory=True),
+                          pairs=torch.empty((max(c.n_quads, 1), 2), dtype=torch.int32, pin_memory=True))
+        sl["sws"] = None
+
+    def submit(self, labels_host: torch.Tensor) -> int:
+        if tuple(labels_host.shape) != self.shape or labels_host.dtype != self.dtype:
+            raise ValueError("labels_host must match the stream's shape and dtype")
+        ticket = self.n
+        sl = self.slots[ticket % self.depth]
+        with torch.cuda.stream(self.s_h2d):
+            if sl["used"]:
+                self.s_h2d.wait_event(sl["ev_comp"])         # the slot's previous volume is processed
+            sl["labels"].copy_(labels_host, non_blocking=True)
+            sl["ev_h2d"].record(self.s_h2d)
+        vol = self.psn.volume(sl["labels"], spacing=self.spacing, origin=self.origin)
+        if sl["ws"] is None:
+            sl["ws"] = self.psn.workspace(vol)
+        self.s_comp.wait_event(sl["ev_h2d"])
+        if sl["used"]:
+            self.s_comp.wait_event(sl["ev_d2h"])               # the slot's previous outputs are read back
+        c = self.psn.count(vol, self.labels, sl["ws"], self.s_comp)   # exact totals (one sync, P:86)
+        self._ensure(sl, c)
+        mesh = self.psn.emit(vol, self.labels, sl["ws"], c, mesh=sl["mesh"], stream=self.s_comp)
+        sl["ev_ext"].record(self.s_comp)
+        if sl["sws"] is None or sl["sws"].numel() < self._sws_bytes(mesh):
+            sl["sws"] = self.psn.smooth_workspace(mesh)
+        out = self.psn.smooth(vol, mesh, self.T, self.lam, self.d, out=sl["out"], ws=sl["sws"], stream=self.s_comp)
+        sl["ev_comp"].record(self.s_comp)
+        P, Q = mesh.n_points, mesh.n_quads
+        host = sl["host"]
+        with torch.cuda.stream(self.s_d2h):
+            self.s_d2h.wait_event(sl["ev_ext"])
+            host["quads"][:Q].copy_(mesh.quads[:Q], non_blocking=True)
+            host["pairs"][:Q].copy_(mesh.pairs[:Q], non_blocking=True)
+            self.s_d2h.wait_event(sl["ev_comp"])
+            host["points"][:P].copy_(out[:P], non_blocking=True)
+            sl["ev_d2h"].record(self.s_d2h)
+        sl["counts"] = (P, Q, mesh.n_stencil)
+        sl["used"] = True
+        self.h2d_bytes = labels_host.numel() * labels_host.element_size()
+        self.d2h_bytes = P * 12 + Q * 24
+        self.n += 1
+        return ticket
+
+    def _sws_bytes(self, mesh) -> int:
+        n = ctypes.c_size_t()
+        self.psn._check(self.psn.L.psn_smooth_workspace(ctypes.byref(mesh.c), ctypes.byref(n)))
+        return n.value
+
+    def result(self, ticket: int):
+        """(points f32 [P,3], quads i32 [Q,4], pairs i32 [Q,2]) on the host for `ticket`."""
+        if not (self.n - self.depth <= ticket < self.n):
+            raise ValueError("ticket no longer (or not yet) available")
+        sl = self.slots[ticket % self.depth]
+        sl["ev_d2h"].synchronize()
+        P, Q, _ = sl["counts"]
+        h = sl["host"]
+        return h["points"][:P], h["quads"][:Q], h["pairs"][:Q]

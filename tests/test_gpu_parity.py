@@ -321,3 +321,36 @@ def test_triangulation_strategies(strategy):
             tris = p.triangulate(mesh, pts, strategy=strategy)
             host = oracle.triangulate(om.quads, pts[:om.n_points].cpu().numpy(), strategy=strategy)
             np.testing.assert_array_equal(gu.u32(tris, 2 * om.n_quads), host)
+
+
+def test_surface_nets_stream_matches_single_calls():
+    """SurfaceNetsStream (pipelined host-buffer API: copy / compute / readback streams, rotating
+    slots) returns, for every submitted volume, exactly the outputs of a plain extraction +
+    smoothing of that volume, also when consecutive volumes differ."""
+    from paper_2401_14906_b200.psn import SurfaceNetsStream
+    p = gu.psn()
+    rng = np.random.default_rng(99)
+    base = psn_gen.generate_host(psn_gen.config("c1"))
+    big = np.zeros_like(base)
+    big[2:-2, 2:-2, 2:-2] = rng.integers(0, 3, size=(28, 28, 28))   # larger totals: slot buffers grow
+    vols = [base, np.roll(base, 3, axis=2), big, np.flip(base, 1).copy(), base, big]
+    sp = (0.8, 1.0, 1.5)
+    T, lam, d = 7, 0.5, 0.5
+    sns = SurfaceNetsStream(p, base.shape, torch.uint16, sp, T, lam, d, depth=2)
+    tickets, expected = [], []
+    for a in vols:
+        h = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        tickets.append(sns.submit(h))
+        _, vol, mesh, _ = gu.gpu_extract(a, spacing=sp)
+        pts = p.smooth(vol, mesh, T, lam, d)
+        expected.append((pts[:mesh.n_points].cpu().numpy(), gu.u32(mesh.quads, mesh.n_quads), gu.u32(mesh.pairs, mesh.n_quads)))
+        if len(tickets) >= 2:
+            t = tickets[-2]
+            pts_h, q_h, pr_h = sns.result(t)
+            e = expected[-2]
+            np.testing.assert_array_equal(pts_h.numpy(), e[0])
+            np.testing.assert_array_equal(q_h.numpy().view(np.uint32), e[1])
+            np.testing.assert_array_equal(pr_h.numpy().view(np.uint32), e[2])
+    pts_h, q_h, pr_h = sns.result(tickets[-1])
+    np.testing.assert_array_equal(pts_h.numpy(), expected[-1][0])
+    np.testing.assert_array_equal(q_h.numpy().view(np.uint32), expected[-1][1])
