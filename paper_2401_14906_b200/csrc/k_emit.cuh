@@ -734,88 +734,110 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
         const int32_t sh_o[3] = {elem_shift(rr0 + rstart[0], 0, 4, 1), elem_shift(rr0 + rstart[1], 0, 4, 1),
                                  elem_shift(rr0 + rstart[2], 0, 4, 1)};
         const int32_t sh_r = elem_shift(rr0, 0, 4, 1);
-        // The warp's work is a stream of ROUNDS (up to 32 points of one of its rows: rows warp,
-        // warp+8, ...).  Software pipelining: the next round's point selection and its 8 corner-label
-        // loads are issued before the current round is emitted, so a round's gather latency overlaps
-        // the previous round's arithmetic and stores.
-        constexpr int WS = kBandThreads / 32;
+        // A warp owns RPWB = 4 CONSECUTIVE rows of the band.  Ids are k-major (reading Q4) and the
+        // scan offsets are in row order, so the warp's points, quads and CSR entries are each ONE
+        // contiguous range: a ROUND takes the next 32 points of that range across row boundaries
+        // (sparse rows share a round), and output positions are the range start plus a running
+        // warp scan.  Software pipelining: the next round's point selection and its 8 corner-label
+        // loads are issued before the current round is emitted.
+        constexpr int RPWB = B / (kBandThreads / 32);
+        const int b0 = warp * RPWB;
+        int32_t rcnt[RPWB];           // points of the warp's rows (0 beyond R)
+        uint32_t rstart[RPWB + 1];    // warp-local index of each row's first point
+        rstart[0] = 0;
+#pragma unroll
+        for (int q = 0; q < RPWB; ++q) {
+            rcnt[q] = (rr0 + b0 + q < R) ? (int32_t)bb.cnt[sh_r + b0 + q] : 0;
+            rstart[q + 1] = rstart[q] + (uint32_t)rcnt[q];
+        }
+        const uint32_t wpts = rstart[RPWB];
+        // (j, k) of the warp's first row; rows b0+q follow by +q with wrap-around
+        const int32_t rf = rr0 + b0;
+        const int32_t jf = rf % NV, kf = kA + rf / NV;
+        const uint32_t offP0 = bb.off[1][sh_o[1] + b0 + 1];                  // window index of the first point
+        const uint32_t qbase0 = bb.offQ[sh_r + b0], sbase0 = bb.offS[sh_r + b0];
         struct Round {
+            uint32_t base, i;
             int32_t b, j, k;
-            uint32_t base, cnt, i;
-            bool valid, act, own;
+            bool act, own;
             uint32_t L[8];   // A, A1, B, B1, C, C1, D, D1 (codes)
         };
-        int32_t pb = warp, pj = 0, pk = 0;   // prepare cursor: row, its (j, k), next round base
-        uint32_t pbase = 0;
-        {
-            const int32_t r = rr0 + pb;
-            pj = r % NV; pk = kA + r / NV;
-        }
-        auto next_row = [&]() {
-            pb += WS; pj += WS;
-            while (pj >= NV) { pj -= NV; ++pk; }
-            pbase = 0;
-        };
-        auto seek = [&]() {   // skip rows without points
-            while (pb < B && rr0 + pb < R && bb.cnt[sh_r + pb] == 0) next_row();
-        };
-        auto prepare = [&](Round &st) {
-            st.valid = pb < B && rr0 + pb < R;
-            if (!st.valid) return;
-            st.b = pb; st.j = pj; st.k = pk; st.base = pbase;
-            st.cnt = bb.cnt[sh_r + pb];
-            st.own = pk >= own0 && pk < own1;
-            const uint32_t t = pbase + lane;
-            st.act = t < st.cnt;
-            // point t of the row: its word = the last word whose first index <= t (prefixes are
-            // non-decreasing; 5-step binary search over the lanes), then the n-th set bit of it
-            const uint32_t wm_l = lane < W32 ? bb.m[1][sh_m[1] + (pb + 1) * W32 + lane] : 0u;
-            const uint32_t wp_l = lane < W32 ? (uint32_t)bb.p[1][sh_p[1] + (pb + 1) * W32 + lane] : 0xFFFFu;
+        auto prepare = [&](Round &st, uint32_t base) {
+            st.base = base;
+            const uint32_t t = base + lane;
+            st.act = t < wpts;
+            int q = 0;
+#pragma unroll
+            for (int qq = 1; qq < RPWB; ++qq) q += (t >= rstart[qq]) ? 1 : 0;
+            uint32_t tr = t;   // index within the row
+#pragma unroll
+            for (int qq = 1; qq < RPWB; ++qq) if (q == qq) tr = t - rstart[qq];
+            const int b = b0 + q;
+            st.b = b;
+            int32_t jj = jf + q, kk = kf;
+            while (jj >= NV) { jj -= NV; ++kk; }   // (tiny NV: several layers per warp)
+            st.j = jj; st.k = kk;
+            st.own = st.act && kk >= own0 && kk < own1;
+            // word of the row holding point tr: the last word whose first index <= tr (prefixes are
+            // non-decreasing; 5-step binary search in shared memory), then the n-th set bit of it
+            const uint16_t *pp = bb.p[1] + sh_p[1] + (b + 1) * W32;
+            const uint32_t *pm = bb.m[1] + sh_m[1] + (b + 1) * W32;
             int wsel = 0;
+            uint32_t mw, pw;
+            const int bfirst = __shfl_sync(kFull, b, 0), blast = __shfl_sync(kFull, b, 31);
+            if (bfirst == blast) {
+                // the round lies in one row (dense rows): lane = plane word, shuffle binary search
+                const uint32_t wm_l = lane < W32 ? pm[lane] : 0u;
+                const uint32_t wp_l = lane < W32 ? (uint32_t)pp[lane] : 0xFFFFu;
 #pragma unroll
-            for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-                const uint32_t pv = __shfl_sync(kFull, wp_l, wsel + s2);
-                if (pv <= t) wsel += s2;
+                for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                    const uint32_t pv = __shfl_sync(kFull, wp_l, wsel + s2);
+                    if (pv <= tr) wsel += s2;
+                }
+                mw = __shfl_sync(kFull, wm_l, wsel); pw = __shfl_sync(kFull, wp_l, wsel);
+                if (!st.act) { mw = 0u; pw = 0u; }
+            } else {
+                // sparse rows share the round: per-lane binary search over its row's staged prefixes
+#pragma unroll
+                for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                    const int c = wsel + s2;
+                    if (c < W32 && (uint32_t)pp[c] <= tr) wsel = c;
+                }
+                mw = st.act ? pm[wsel] : 0u; pw = st.act ? (uint32_t)pp[wsel] : 0u;
             }
-            const uint32_t mw = __shfl_sync(kFull, wm_l, wsel), pw = __shfl_sync(kFull, wp_l, wsel);
-            uint32_t nth = t - pw, bitpos = 0;   // position of the nth (0-based) set bit of mw
+            uint32_t nth = tr - pw, bitpos = 0, rest = mw;   // position of the nth (0-based) set bit of mw
 #pragma unroll
             for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-                const uint32_t lo = __popc(mw & ((1u << (bitpos + s2)) - 1u) & ~((1u << bitpos) - 1u));
-                if (lo <= nth) { nth -= lo; bitpos += s2; }
+                const uint32_t lo = __popc(rest & ((1u << s2) - 1u));
+                if (lo <= nth) { nth -= lo; bitpos += s2; rest >>= s2; }
             }
             st.i = st.act ? (uint32_t)(wsel * 32 + bitpos) : 0u;
-            if (st.act && st.own) {
-                const T *pA = lab + ((size_t)(pk - (int32_t)a.z_lo) * N + pj) * M + st.i;   // rows j, j+1 of slices k, k+1
+            if (st.own) {
+                const T *pA = lab + ((size_t)(kk - (int32_t)a.z_lo) * N + jj) * M + st.i;   // rows j, j+1 of slices k, k+1
                 const T *pB = pA + M, *pC = pA + (size_t)N * M, *pD = pC + M;
                 st.L[0] = code_at<T, ANZ>(pA, ls); st.L[1] = code_at<T, ANZ>(pA + 1, ls);
                 st.L[2] = code_at<T, ANZ>(pB, ls); st.L[3] = code_at<T, ANZ>(pB + 1, ls);
                 st.L[4] = code_at<T, ANZ>(pC, ls); st.L[5] = code_at<T, ANZ>(pC + 1, ls);
                 st.L[6] = code_at<T, ANZ>(pD, ls); st.L[7] = code_at<T, ANZ>(pD + 1, ls);
             }
-            pbase += 32;
-            if (pbase >= st.cnt) { next_row(); seek(); }
         };
         // neighbour row q -> (range, index offset from b)
         const int nq_g[5] = {0, 0, 1, 1, 2};
         const int nq_d[5] = {0, 1, 0, 2, 0};
         uint32_t run_q = 0, run_s = 0;
-        seek();
         Round cur;
-        prepare(cur);
-        while (cur.valid) {
+        if (wpts) prepare(cur, 0);
+        for (uint32_t base = 0; base < wpts; base += 32) {
             Round nxt;
-            prepare(nxt);
+            if (base + 32 < wpts) prepare(nxt, base + 32);
             const int32_t b = cur.b, j = cur.j, k = cur.k;
             const int32_t i = (int32_t)cur.i;
             const bool act = cur.act, own = cur.own;
-            if (cur.base == 0) { run_q = 0; run_s = 0; }
-            const uint32_t offP = bb.off[1][sh_o[1] + b + 1];
             const uint32_t t = cur.base + lane;
-            const uint32_t wi = offP + t;
+            const uint32_t wi = offP0 + t;
             const uint32_t g = gid_base + wi;
             uint32_t fm = 0, qb = 0, cA = 0, cA1 = 0, cB = 0, cC = 0;
-            if (act && own) {
+            if (own) {
                 const uint32_t A = cur.L[0], A1 = cur.L[1], Bv = cur.L[2], B1 = cur.L[3];
                 const uint32_t C = cur.L[4], C1 = cur.L[5], D = cur.L[6], D1 = cur.L[7];
                 const bool XA = A != A1, XB = Bv != B1, XC = C != C1, XD = D != D1;
@@ -837,12 +859,13 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
             const uint32_t x = scan3(packed, lane);
             const uint32_t tot = __shfl_sync(kFull, x, 31);
             const uint32_t ex = x - packed;
+            const bool stage = (tot & 0xffffu) >= kStageCsr;   // dense round: CSR ids through shared memory
             if (act) {
                 a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
                 a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
                 a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
             }
-            if (act && own) {
+            if (own) {
                 const uint32_t wl = (uint32_t)i >> 5, below = (1u << (i & 31)) - 1u;
                 // neighbour ids actually referenced by this point's stencil entries / quads
                 const uint32_t need = ((qb & 1u) ? 1u : 0u) | (((fm & 1u) || (qb & 3u)) ? 2u : 0u) |
@@ -857,21 +880,18 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
                                                      __popc(bb.m[gg][e + sh_m[gg]] & below)
                                                : 0u;
                 }
-                const uint32_t qbase = bb.offQ[sh_r + b], sbase = bb.offS[sh_r + b];
                 const uint32_t o = wi - halo_lo;
+                const uint32_t s0 = sbase0 + run_s + (ex & 0xffffu);
                 a.fmask[o] = (uint8_t)fm;
-                a.csr_off[o] = a.first_stencil + sbase + run_s + (ex & 0xffffu);
-                // dense rounds stage their CSR ids (face order) for a coalesced copy-out below;
-                // sparse rounds store them directly
-                uint32_t *sc = (tot & 0xffffu) >= kStageCsr ? scsr[warp] + (ex & 0xffffu)
-                                                             : a.csr_ids + sbase + run_s + (ex & 0xffffu);
+                a.csr_off[o] = a.first_stencil + s0;
+                uint32_t *sc = stage ? scsr[warp] + (ex & 0xffffu) : a.csr_ids + s0;
                 if (fm & 1u) *sc++ = gn[1];      // -z  (j, k-1)
                 if (fm & 2u) *sc++ = gn[2];      // -y  (j-1, k)
                 if (fm & 4u) *sc++ = g - 1u;     // -x
                 if (fm & 8u) *sc++ = g + 1u;     // +x
                 if (fm & 16u) *sc++ = gn[3];     // +y  (j+1, k)
                 if (fm & 32u) *sc++ = gn[4];     // +z  (j, k+1)
-                uint32_t qs = qbase + run_q + (ex >> 16);
+                uint32_t qs = qbase0 + run_q + (ex >> 16);
                 if (qb & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
                     *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[0], gn[1], g, gn[2]);
                     *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cA1);
@@ -888,13 +908,11 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
                     ++qs;
                 }
             }
-            {   // the round's CSR ids are one contiguous range: coalesced copy-out
+            if (stage) {   // the round's CSR ids are one contiguous range: coalesced copy-out
                 const uint32_t ns = tot & 0xffffu;
                 __syncwarp();
-                if (own && ns >= kStageCsr) {
-                    uint32_t *dst = a.csr_ids + bb.offS[sh_r + b] + run_s;
-                    for (uint32_t e = lane; e < ns; e += 32) dst[e] = scsr[warp][e];
-                }
+                uint32_t *dst = a.csr_ids + sbase0 + run_s;
+                for (uint32_t e = lane; e < ns; e += 32) dst[e] = scsr[warp][e];
                 __syncwarp();
             }
             run_q += tot >> 16;
