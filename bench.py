@@ -250,7 +250,9 @@ def run_psn(args, rank, world, local_rank):
         tab = pipe.table
         P, Q, S = (int(x) for x in tab[:, :3].sum(0))
         run_extract = pipe.extract
-        run_smooth = pipe.smooth
+        # smoothing on point-balanced shards (C4): equal slabs leave c4's per-rank point counts at
+        # up to 1.5x the mean at 8 ranks; --no-balance keeps the extraction slabs
+        run_smooth = pipe.smooth if args.no_balance else pipe.smooth_balanced
     torch.cuda.synchronize()
 
     def barrier():
@@ -366,7 +368,8 @@ def run_psn(args, rank, world, local_rank):
             "dtype": {1: "u8", 2: "u16", 4: "u32"}[b] + "/f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[cfg], "dims": [M, N, O], "label_bytes": b, "iterations": T,
                        "relaxation": lam, "constraint_voxels": d, "spacing": list(sp),
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"z-slab x{world}" + ("" if args.no_balance else ", point-balanced smoothing"))
+                       if world > 1 else "single GPU",
                        "l2": ("inputs larger than L2 (%.2f GB labels, %.2f GB smoothing state)" % (V * b / 1e9, P * 28 / 1e9))
                        if V * b > l2 else "inputs fit in L2 (no flush; absolute numbers only)"},
             "counts": {"points": P, "quads": Q, "stencil": S},
@@ -390,6 +393,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="psn", choices=["psn", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-balance", action="store_true", help="N > 1: smooth on the extraction slabs (no C4 re-cut)")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-voxels", type=float, default=96e6, help="oracle sample size for cpu_baseline (~10-30 s)")

@@ -14,12 +14,19 @@ interior side).  The path has two real exchange steps:
       (its lower halo).  The exchange after the last iteration is the final
       halo refresh (C3) needed by triangulation.
 
+  C4  (balance=True) once per step after extraction: the point-balanced
+      re-partition of the smoothing work (balance.py): equal global-id shares,
+      the moved points' face masks / CSR rows / anchors sent point-to-point to
+      their new owners; C2 then runs on the re-cut windows.
+
 The collectives use torch.distributed (NCCL on GPUs; gloo in the CPU tests).
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+
+from . import balance
 
 
 def partition(n_layers: int, world: int):
@@ -129,6 +136,15 @@ class SlabPipeline:
         self.psn.emit(self.vol, self.labels, self.ws, c, first=(self.first_point, self.first_quad, self.first_stencil),
                       mesh=self.mesh, stream=stream)
 
+    def smooth_balanced(self, stream=None):
+        """C4 (point-balanced re-partition of this step's mesh) + T Jacobi steps on the
+        re-cut shards with their halo exchange; returns this rank's share of the
+        global smoothed points (ids [cuts[rank], cuts[rank+1]))."""
+        total = int(self.table[:, 0].sum())
+        self.balanced = BalancedSmoother(self.psn, self.vol, self.mesh, self.first_point, self.first_stencil, total,
+                                         self.T, self.lam, self.d, self.group)
+        return self.balanced.smooth(stream)
+
     def smooth(self, stream=None):
         """T Jacobi steps with a halo exchange after each (C2; the last one is C3)."""
         src = None
@@ -140,3 +156,85 @@ class SlabPipeline:
             src = dst
         self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, 0, self.mesh.n_window, stream)
         return self.out
+
+
+def p2p_transport(group=None):
+    """balance.assemble transport over torch.distributed point-to-point (blocking
+    send / recv in the common move order: every move involves exactly its two
+    ranks, so the sequence cannot deadlock)."""
+    me = dist.get_rank(group)
+
+    def transport(src, dst, tensor, like):
+        if src == dst:
+            return tensor if me == src else None
+        if me == src:
+            dist.send(tensor, dst, group=group)
+            return None
+        if me == dst:
+            dist.recv(like, src, group=group)
+            return like
+        return None
+    return transport
+
+
+def shard_halo_exchange(buf: torch.Tensor, shard_windows, moves, rank: int, group=None):
+    """C2 on re-cut windows: for every halo move (src, dst, g0, g1), src sends its
+    window slice of ids [g0, g1) to dst's window slice (batched P2P)."""
+    ops = []
+    for (s, d, g0, g1) in moves:
+        if s == rank:
+            w0 = shard_windows[s][0]
+            ops.append(dist.P2POp(dist.isend, buf[g0 - w0:g1 - w0], d, group))
+        elif d == rank:
+            w0 = shard_windows[d][0]
+            ops.append(dist.P2POp(dist.irecv, buf[g0 - w0:g1 - w0], s, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+
+class BalancedSmoother:
+    """C4 + smoothing on the point-balanced shards: built from a
+    rank's extraction (SlabPipeline) after C1; smooth() runs T psn_smooth_step
+    iterations with the halo exchange of the re-cut windows and returns the
+    world coordinates of this rank's own ids [cuts[rank], cuts[rank+1])."""
+
+    def __init__(self, psn, vol, mesh, first_point: int, first_stencil: int, total_points: int, iterations: int,
+                 relaxation: float, constraint: float, group=None):
+        self.psn, self.vol, self.group = psn, vol, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.T, self.lam, self.d = iterations, relaxation, constraint
+        dev = mesh.points.device
+        src = balance.source_from_mesh(mesh, first_point, first_stencil)
+        owned = torch.tensor([first_point, mesh.n_points], dtype=torch.int64, device=dev)
+        allo = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(allo, owned, group=group)
+        owned_all = [tuple(int(x) for x in allo[2 * r:2 * r + 2].tolist()) for r in range(self.world)]
+        self.cuts = balance.balanced_cuts(total_points, self.world)
+        moves = balance.plan_moves(owned_all, self.cuts)
+        self.shard = balance.assemble(self.rank, self.cuts, moves, src, p2p_transport(group), dev)
+        win = torch.tensor([self.shard.w0, self.shard.w1], dtype=torch.int64, device=dev)
+        allw = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(allw, win, group=group)
+        self.windows = [tuple(int(x) for x in allw[2 * r:2 * r + 2].tolist()) for r in range(self.world)]
+        self.halo = balance.halo_moves(self.cuts, self.windows)
+        self.mesh = balance.shard_mesh(psn, self.shard)
+        nw = max(self.shard.w1 - self.shard.w0, 1)
+        self.sws = psn.smooth_workspace(self.mesh)
+        self.buf = [torch.zeros((nw, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.out = torch.empty((nw, 3), dtype=torch.float32, device=dev)
+
+    def smooth(self, stream=None):
+        sh = self.shard
+        src = None
+        if sh.n_points:
+            self.psn.smooth_prepare(self.mesh, self.sws, stream)
+        for t in range(self.T):
+            dst = self.buf[t & 1]
+            if sh.n_points:
+                self.psn.smooth_step(self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+            shard_halo_exchange(dst, self.windows, self.halo, self.rank, self.group)
+            src = dst
+        if sh.n_points:
+            self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, sh.halo_lo, sh.halo_lo + sh.n_points, stream)
+        return self.out[sh.halo_lo:sh.halo_lo + sh.n_points]
