@@ -208,6 +208,24 @@ def test_degenerate_and_errors():
     with pytest.raises(PSNError) as e:
         p.smooth(vol, mesh, 3, 1.5, 0.5)
     assert e.value.status == PSN_ERR_ARG
+    for fn, bad in ((p.set_counting, 2), (p.set_emission, 3), (p.set_constraint, 2), (p.set_smoothing, 5)):
+        with pytest.raises(PSNError) as e:
+            fn(bad)
+        assert e.value.status == PSN_ERR_ARG
+    with pytest.raises(PSNError) as e:
+        p.triangulate(mesh, mesh.points, strategy=4)
+    assert e.value.status == PSN_ERR_ARG
+    # the slab smoothing step supports the box constraint only
+    try:
+        p.set_constraint(1)
+        ws = p.smooth_workspace(mesh)
+        p.smooth_prepare(mesh, ws)
+        dst = torch.empty_like(mesh.points)
+        with pytest.raises(PSNError) as e:
+            p.smooth_step(mesh, ws, None, dst, 0.5, 0.5)
+        assert e.value.status == PSN_ERR_ARG
+    finally:
+        p.set_constraint(0)
 
 
 def test_smoothing_zero_iterations_is_anchors():
