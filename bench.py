@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """bench.py -- PSN hot path on B200: extraction (k_count3 -> k_scan -> k_emit_band) +
-T-iteration constrained smoothing (k_smooth_prep + T x k_smooth_soa), timed with CUDA events.
+T-iteration constrained smoothing (k_smooth_prep + T x k_smooth_v4), timed with CUDA events.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl psn|reference]
 
@@ -306,18 +306,18 @@ def run_psn(args, rank, world, local_rank):
     ext_vps = V / (t_ext * 1e-3)
     sm_ptit = P * T / (t_sm * 1e-3)
     ext_gbs = b_ext / (t_ext * 1e-3) / 1e9
-    # dominant kernel: k_smooth_soa (T launches per step) -- achieved = B_sm per launch / avg launch time,
+    # dominant kernel: k_smooth_v4 (T launches per step) -- achieved = B_sm per launch / avg launch time,
     # the launch time taken as (psn_smooth time incl. the one-off k_smooth_prep) / T (conservative)
     per_launch_ms = t_sm / max(T, 1)
     sm_gbs = b_sm / (per_launch_ms * 1e-3) / 1e9
-    dominant = "k_smooth_soa" if t_sm >= t_ext else "extraction (k_count3+k_scan+k_emit_band)"
-    roof = {"bound": "hbm", "kernel": "k_smooth_soa", "achieved": sm_gbs / world, "peak": peak, "unit": "GB/s",
-            "frac": sm_gbs / world / peak, "traffic": profile_traffic("k_smooth_soa", cfg), "peak_source": peak_src,
+    dominant = "k_smooth_v4" if t_sm >= t_ext else "extraction (k_count3+k_scan+k_emit_band)"
+    roof = {"bound": "hbm", "kernel": "k_smooth_v4", "achieved": sm_gbs / world, "peak": peak, "unit": "GB/s",
+            "frac": sm_gbs / world / peak, "traffic": profile_traffic("k_smooth_v4", cfg), "peak_source": peak_src,
             "bytes_per_launch": b_sm / world, "launch_ms": per_launch_ms,
-            "note": "achieved = algorithmic bytes per launch (24P + 4(P+1) + 4S, per GPU) / average k_smooth_soa launch "
+            "note": "achieved = algorithmic bytes per launch (24P + 4(P+1) + 4S, per GPU) / average k_smooth_v4 launch "
                     "time (CUDA events around psn_smooth -- the T back-to-back launches plus the one-off smoothing-cache "
                     "prep -- divided by T)"}
-    if dominant != "k_smooth_soa":
+    if dominant != "k_smooth_v4":
         roof["note"] += "; extraction dominated this config's step, see extract.frac"
 
     # ---------------------------------------------------------------- e2e through the public host-buffer API

@@ -239,30 +239,26 @@ __global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
     }
 }
 
-// One Jacobi step on STRUCTURE-OF-ARRAYS offsets (x[W] | y[W] | z[W], stride
-// `ws` floats): one point per thread, so every gather instruction of a warp
-// reads consecutive floats of one array (the AoS float3 layout needs three
-// sector-straddling scalar loads per gather).  +-x neighbours (w-1, w+1) come
-// from the adjacent lanes; lanes 0 / 31 and the last point load them.  The
-// arithmetic is jacobi_update: bit-identical to k_smooth.
-struct SmoothSoA {
-    const float *src;          // SoA window offsets; NULL = all zero (first iteration)
-    float *dst;                // SoA window offsets (own entries written)
+// One Jacobi step on float4 offsets (x, y, z, unused): one 16-byte load per
+// gathered neighbour instead of three scalar loads (the kernel is issue-bound,
+// not DRAM-bound, so the extra 4 bytes per point cost less than the saved
+// instructions).  Same arithmetic as k_smooth / k_smooth_tb (bit-identical).
+struct SmoothV4 {
+    const float4 *src;         // window offsets; NULL = all zero (first iteration)
+    float4 *dst;
     float *world;              // if non-NULL: write AoS world coordinates here instead of dst
-    const uint8_t *fmask;
     const uint4 *nbr;
     const float *points;
-    uint32_t n_own, halo_lo, ws;
+    uint32_t n_own, halo_lo;
     float lambda, d;
     double sp[3], org[3];
 };
 
-__global__ void __launch_bounds__(256) k_smooth_soa(SmoothSoA a) {
+__global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
-    const uint32_t n = a.n_own, ws = a.ws;
-    const float *__restrict__ sx = a.src, *__restrict__ sy = a.src + ws, *__restrict__ sz = a.src + 2 * ws;
+    const uint32_t n = a.n_own;
+    const float4 *__restrict__ src = a.src;
     const uint32_t stride = gridDim.x * blockDim.x;
-    // uniform trip count so that every lane takes part in the shuffles
     for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
         const uint32_t i = base + lane;
         const bool act = i < n;
@@ -271,35 +267,34 @@ __global__ void __launch_bounds__(256) k_smooth_soa(SmoothSoA a) {
         const uint4 nbw = __ldg(a.nbr + ii);
         const uint32_t f = act ? nbr_faces(nbw) : 0u;
         const uint4 nb = nbr_idx(nbw);
-        float3 o = make_float3(0.f, 0.f, 0.f), g0 = o, g1 = o, g2 = o, g3 = o;
-        if (a.src) {
-            o = make_float3(__ldg(sx + w), __ldg(sy + w), __ldg(sz + w));
-            g0 = make_float3(__ldg(sx + nb.x), __ldg(sy + nb.x), __ldg(sz + nb.x));
-            g1 = make_float3(__ldg(sx + nb.y), __ldg(sy + nb.y), __ldg(sz + nb.y));
-            g2 = make_float3(__ldg(sx + nb.z), __ldg(sy + nb.z), __ldg(sz + nb.z));
-            g3 = make_float3(__ldg(sx + nb.w), __ldg(sy + nb.w), __ldg(sz + nb.w));
+        float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f), h0 = o4, h1 = o4, h2 = o4, h3 = o4;
+        if (src) {
+            o4 = __ldg(src + w);
+            h0 = __ldg(src + nb.x); h1 = __ldg(src + nb.y); h2 = __ldg(src + nb.z); h3 = __ldg(src + nb.w);
         }
+        const float3 o = make_float3(o4.x, o4.y, o4.z);
         float3 mx, px;
         mx.x = __shfl_up_sync(kFull, o.x, 1); mx.y = __shfl_up_sync(kFull, o.y, 1); mx.z = __shfl_up_sync(kFull, o.z, 1);
         px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
         if (!act) continue;
-        if (a.src && f) {
-            if ((f & 4u) && lane == 0) mx = make_float3(__ldg(sx + w - 1u), __ldg(sy + w - 1u), __ldg(sz + w - 1u));
-            if ((f & 8u) && (lane == 31 || i + 1u >= n)) px = make_float3(__ldg(sx + w + 1u), __ldg(sy + w + 1u), __ldg(sz + w + 1u));
+        if (src && f) {
+            if ((f & 4u) && lane == 0) { const float4 v = __ldg(src + w - 1u); mx = make_float3(v.x, v.y, v.z); }
+            if ((f & 8u) && (lane == 31 || i + 1u >= n)) { const float4 v = __ldg(src + w + 1u); px = make_float3(v.x, v.y, v.z); }
         }
-        const float3 r = jacobi_update_box(f, o, mx, px, g0, g1, g2, g3, a.lambda, a.d);
+        const float3 r = jacobi_update_box(f, o, mx, px, make_float3(h0.x, h0.y, h0.z), make_float3(h1.x, h1.y, h1.z),
+                                           make_float3(h2.x, h2.y, h2.z), make_float3(h3.x, h3.y, h3.z), a.lambda, a.d);
         if (a.world) {
             a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
             a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
             a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
         } else {
-            a.dst[w] = r.x; a.dst[ws + w] = r.y; a.dst[2 * ws + w] = r.z;
+            a.dst[w] = make_float4(r.x, r.y, r.z, 0.f);
         }
     }
 }
 
 // Same step with the sphere constraint (separate kernel: the box kernel stays minimal).
-struct SmoothSoASphere {   // k_smooth_soa_sphere: as SmoothSoA plus the sphere (reading Q26)
+struct SmoothSoASphere {   // k_smooth_soa_sphere: SoA offsets, sphere constraint (reading Q26)
     const float *src;          // SoA window offsets; NULL = all zero (first iteration)
     float *dst;                // SoA window offsets (own entries written)
     float *world;              // if non-NULL: write AoS world coordinates here instead of dst

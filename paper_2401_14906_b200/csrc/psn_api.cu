@@ -607,37 +607,47 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     }
     if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
-        // one launch per Jacobi iteration: SoA offset buffers in the two buffer slots
-        float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
+        // one launch per Jacobi iteration, offsets double-buffered in the two buffer slots
         const Constraint cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
-        SmoothSoA a;
+        if (!cons.sphere) {   // box constraint: float4 offsets (one 16-byte load per gather)
+            SmoothV4 v;
+            memset(&v, 0, sizeof(v));
+            v.nbr = static_cast<const uint4 *>(ws); v.points = mesh->points;
+            v.n_own = (uint32_t)mesh->n_points; v.halo_lo = (uint32_t)mesh->halo_lo_points;
+            v.lambda = relaxation; v.d = constraint_distance;
+            for (int c = 0; c < 3; ++c) { v.sp[c] = vol->spacing[c]; v.org[c] = vol->origin[c]; }
+            float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
+            int occ4 = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_smooth_v4, 256, 0);
+            const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ4, 1)));
+            const float4 *s4 = nullptr;
+            for (int32_t t = 0; t < iterations; ++t) {
+                const bool last = (t == iterations - 1);
+                v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
+                k_smooth_v4<<<(unsigned)g4, 256, 0, st>>>(v);
+                ++ctx->launches;
+                s4 = v.dst;
+            }
+            return cuda_check(ctx, "smooth launch");
+        }
+        // sphere constraint: SoA offsets (k_smooth_soa_sphere)
         SmoothSoASphere b;
-        memset(&a, 0, sizeof(a));
         memset(&b, 0, sizeof(b));
-        a.fmask = mesh->face_masks; a.nbr = static_cast<const uint4 *>(ws); a.points = mesh->points;
-        a.n_own = (uint32_t)mesh->n_points; a.halo_lo = (uint32_t)mesh->halo_lo_points;
-        a.ws = (uint32_t)soa_stride(SL.nw);
-        a.lambda = relaxation; a.d = constraint_distance;
-        for (int c = 0; c < 3; ++c) { a.sp[c] = vol->spacing[c]; a.org[c] = vol->origin[c]; }
-        b.fmask = a.fmask; b.nbr = a.nbr; b.points = a.points; b.n_own = a.n_own; b.halo_lo = a.halo_lo; b.ws = a.ws;
+        b.fmask = mesh->face_masks; b.nbr = static_cast<const uint4 *>(ws); b.points = mesh->points;
+        b.n_own = (uint32_t)mesh->n_points; b.halo_lo = (uint32_t)mesh->halo_lo_points;
+        b.ws = (uint32_t)soa_stride(SL.nw);
         b.lambda = relaxation; b.cons = cons;
-        for (int c = 0; c < 3; ++c) { b.sp[c] = a.sp[c]; b.org[c] = a.org[c]; }
+        for (int c = 0; c < 3; ++c) { b.sp[c] = vol->spacing[c]; b.org[c] = vol->origin[c]; }
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cons.sphere ? (const void *)k_smooth_soa_sphere
-                                                                        : (const void *)k_smooth_soa, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_smooth_soa_sphere, 256, 0);
         const int64_t gsoa = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
+        float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
         const float *src = nullptr;
         for (int32_t t = 0; t < iterations; ++t) {
             const bool last = (t == iterations - 1);
             float *dst = last ? nullptr : buf[t & 1];
-            float *world = last ? out : nullptr;
-            if (cons.sphere) {
-                b.src = src; b.dst = dst; b.world = world;
-                k_smooth_soa_sphere<<<(unsigned)gsoa, 256, 0, st>>>(b);
-            } else {
-                a.src = src; a.dst = dst; a.world = world;
-                k_smooth_soa<<<(unsigned)gsoa, 256, 0, st>>>(a);
-            }
+            b.src = src; b.dst = dst; b.world = last ? out : nullptr;
+            k_smooth_soa_sphere<<<(unsigned)gsoa, 256, 0, st>>>(b);
             ++ctx->launches;
             src = dst;
         }
