@@ -715,15 +715,46 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
         (void)bytes;
     };
 
-    int32_t band = blockIdx.x;
-    if (band < nbands && tid == 0) issue(band, 0);
+    // Bands without points (outside the surfaces; most of a sparse volume) are skipped without
+    // staging: warp 0 looks 32 of the CTA's bands ahead at once (band b has points iff the
+    // window offsets of its first and one-past-last rows differ) and stages the next non-empty one.
+    const int32_t G = (int32_t)gridDim.x;
+    auto next_band = [&](int32_t c) -> int32_t {   // warp 0, all lanes; nbands if none
+        for (int32_t base = c; base < nbands; base += 32 * G) {
+            const int32_t cand = base + lane * G;
+            bool ne = false;
+            if (cand < nbands) {
+                const int32_t r0 = cand * B, r1 = min(r0 + B, R) - 1;
+                ne = __ldg(a.offP + r1) + __ldg(a.cntP + r1) != __ldg(a.offP + r0);
+            }
+            const uint32_t bal = __ballot_sync(kFull, ne);
+            if (bal) return base + (__ffs(bal) - 1) * G;
+        }
+        return nbands;
+    };
+    __shared__ int32_t s_nb[2];
+    if (warp == 0) {
+        const int32_t b0 = next_band(blockIdx.x);
+        if (lane == 0) {
+            s_nb[0] = b0;
+            if (b0 < nbands) issue(b0, 0);
+        }
+    }
     uint32_t par[2] = {0u, 0u};
-    for (int it = 0; band < nbands; band += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+        __syncthreads();   // every thread is past the previous band (its buffer may be refilled) and s_nb is set
+        const int32_t band = s_nb[it & 1];
+        if (band >= nbands) break;
         const int sb = it & 1;
+        if (warp == 0) {
+            const int32_t nb = next_band(band + G);
+            if (lane == 0) {
+                s_nb[sb ^ 1] = nb;
+                if (nb < nbands) issue(nb, sb ^ 1);
+            }
+        }
         mbar_wait(&bar[sb], par[sb]);
         par[sb] ^= 1u;
-        __syncthreads();   // every thread is past the previous band: its buffer may be refilled
-        if (tid == 0 && band + (int32_t)gridDim.x < nbands) issue(band + gridDim.x, sb ^ 1);
         const BandBuf &bb = buf[sb];
         const int32_t rr0 = band * B;
         // staged-row accessors (element shifts of each range's aligned copy)
