@@ -247,13 +247,51 @@ struct SmoothV4 {
     const float4 *src;         // window offsets; NULL = all zero (first iteration)
     float4 *dst;
     float *world;              // if non-NULL: write AoS world coordinates here instead of dst
-    const uint4 *nbr;
+    const uint4 *nbr;          // smoothing cache (k_smooth_prep), or
+    const uint2 *nbr8;         // its packed form (k_smooth_prep8) when the volume's rows / layers allow
     const float *points;
     uint32_t n_own, halo_lo;
     float lambda, d;
     double sp[3], org[3];
 };
 
+// Packed smoothing cache, 8 bytes per point (k_smooth_prep8): the id DISTANCES
+// to the -z, +z (21 bits each), -y, +y (10 bits each) neighbours -- 0 = no
+// such face, the slot then names the point itself -- and the -x / +x face
+// bits.  Ids are k-major (reading Q4), so a y neighbour is at most one row of
+// cells away (<= M-1 ids) and a z neighbour at most one layer ((M-1)(N-1));
+// the host selects this form when M-1 < 2^10 and (M-1)(N-1) < 2^21.
+//   lo = dmz | dpz << 21            hi = dpz >> 11 | dmy << 10 | dpy << 20 | fx << 30
+__device__ __forceinline__ uint2 nbr8_pack(uint32_t w, uint4 v, uint32_t f) {
+    const uint32_t dmz = w - v.x, dmy = w - v.y, dpy = v.z - w, dpz = v.w - w;
+    return make_uint2(dmz | (dpz << 21), (dpz >> 11) | (dmy << 10) | (dpy << 20) | (((f >> 2) & 3u) << 30));
+}
+__device__ __forceinline__ void nbr8_unpack(uint2 e, uint32_t w, uint32_t &f, uint4 &nb) {
+    const uint32_t dmz = e.x & 0x1FFFFFu, dpz = __funnelshift_r(e.x, e.y, 21) & 0x1FFFFFu;
+    const uint32_t dmy = (e.y >> 10) & 0x3FFu, dpy = (e.y >> 20) & 0x3FFu;
+    f = (dmz ? 1u : 0u) | (dmy ? 2u : 0u) | ((e.y >> 30) << 2) | (dpy ? 16u : 0u) | (dpz ? 32u : 0u);
+    nb = make_uint4(w - dmz, w - dmy, w + dpy, w + dpz);
+}
+
+__global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, const uint32_t *csr_off,
+                                                      const uint32_t *csr_ids, uint2 *nbr8, int64_t n_own,
+                                                      uint32_t halo_lo, uint32_t win_base, uint32_t first_stencil) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_own; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = fmask[i];
+        const uint32_t w = halo_lo + (uint32_t)i;
+        uint32_t s = csr_off[i] - first_stencil;
+        uint4 v = make_uint4(w, w, w, w);
+        if (f & 1u) v.x = csr_ids[s++] - win_base;    // -z
+        if (f & 2u) v.y = csr_ids[s++] - win_base;    // -y
+        if (f & 4u) ++s;                              // -x  (w - 1)
+        if (f & 8u) ++s;                              // +x  (w + 1)
+        if (f & 16u) v.z = csr_ids[s++] - win_base;   // +y
+        if (f & 32u) v.w = csr_ids[s++] - win_base;   // +z
+        nbr8[i] = nbr8_pack(w, v, f);
+    }
+}
+
+template <bool PACKED>
 __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
@@ -264,9 +302,16 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
         const bool act = i < n;
         const uint32_t ii = act ? i : n - 1u;
         const uint32_t w = a.halo_lo + ii;
-        const uint4 nbw = __ldg(a.nbr + ii);
-        const uint32_t f = act ? nbr_faces(nbw) : 0u;
-        const uint4 nb = nbr_idx(nbw);
+        uint32_t f;
+        uint4 nb;
+        if (PACKED) {
+            nbr8_unpack(__ldg(a.nbr8 + ii), w, f, nb);
+        } else {
+            const uint4 nbw = __ldg(a.nbr + ii);
+            f = nbr_faces(nbw);
+            nb = nbr_idx(nbw);
+        }
+        if (!act) f = 0u;
         float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f), h0 = o4, h1 = o4, h2 = o4, h3 = o4;
         if (src) {
             o4 = __ldg(src + w);

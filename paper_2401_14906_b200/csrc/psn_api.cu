@@ -605,26 +605,40 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         ++ctx->launches;
         return cuda_check(ctx, "finalize launch");
     }
-    if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
+    const Constraint cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
+    // packed 8-byte smoothing cache: y neighbours are < M ids away, z neighbours < (M-1)(N-1)
+    const int64_t Mc = vol->dims[0] - 1, Nc = vol->dims[1] - 1;
+    const bool packed = ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION && !cons.sphere && Mc < (1 << 10) &&
+                        Mc * Nc < (1 << 21) && !getenv("PSN_SMOOTH_NBR16");
+    if (packed) {
+        k_smooth_prep8<<<(unsigned)grid_for(ctx, nw), 256, 0, st>>>(
+            mesh->face_masks, mesh->stencil_offsets, mesh->stencil_ids, static_cast<uint2 *>(ws), nw,
+            (uint32_t)mesh->halo_lo_points, (uint32_t)(mesh->first_point - mesh->halo_lo_points),
+            (uint32_t)mesh->first_stencil);
+        ++ctx->launches;
+        if ((s = cuda_check(ctx, "smooth prep launch")) != PSN_OK) return s;
+    } else if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) {
+        return s;
+    }
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
         // one launch per Jacobi iteration, offsets double-buffered in the two buffer slots
-        const Constraint cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
         if (!cons.sphere) {   // box constraint: float4 offsets (one 16-byte load per gather)
             SmoothV4 v;
             memset(&v, 0, sizeof(v));
-            v.nbr = static_cast<const uint4 *>(ws); v.points = mesh->points;
+            v.nbr = static_cast<const uint4 *>(ws); v.nbr8 = static_cast<const uint2 *>(ws); v.points = mesh->points;
             v.n_own = (uint32_t)mesh->n_points; v.halo_lo = (uint32_t)mesh->halo_lo_points;
             v.lambda = relaxation; v.d = constraint_distance;
             for (int c = 0; c < 3; ++c) { v.sp[c] = vol->spacing[c]; v.org[c] = vol->origin[c]; }
             float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
             int occ4 = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_smooth_v4, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, packed ? k_smooth_v4<true> : k_smooth_v4<false>, 256, 0);
             const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ4, 1)));
             const float4 *s4 = nullptr;
             for (int32_t t = 0; t < iterations; ++t) {
                 const bool last = (t == iterations - 1);
                 v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
-                k_smooth_v4<<<(unsigned)g4, 256, 0, st>>>(v);
+                if (packed) k_smooth_v4<true><<<(unsigned)g4, 256, 0, st>>>(v);
+                else k_smooth_v4<false><<<(unsigned)g4, 256, 0, st>>>(v);
                 ++ctx->launches;
                 s4 = v.dst;
             }

@@ -280,6 +280,26 @@ def test_wavefront_smoothing_bit_identical(G, tile):
         p.set_smoothing(1, 0, 0)
 
 
+def test_packed_smoothing_cache_bit_identical(monkeypatch):
+    """The packed 8-byte smoothing cache (id distances, chosen when M-1 < 2^10 and
+    (M-1)(N-1) < 2^21) gives the same bits as the 16-byte one, including a volume at
+    the packing limits (rows of 1023 cells: y distances up to 1022; dense layers)."""
+    p = gu.psn()
+    rng = np.random.default_rng(77)
+    vols = [rng.integers(0, 4, size=(12, 40, 60)).astype(np.uint8),
+            rng.integers(0, 3, size=(4, 9, 1024)).astype(np.uint16),
+            psn_gen.generate_host(psn_gen.config("c2"))[100:140]]
+    for a in vols:
+        _, vol, mesh, _ = gu.gpu_extract(a, spacing=(0.8, 1.0, 1.5))
+        ws = p.smooth_workspace(mesh)
+        packed = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws).clone()
+        monkeypatch.setenv("PSN_SMOOTH_NBR16", "1")
+        wide = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws)
+        monkeypatch.delenv("PSN_SMOOTH_NBR16")
+        n = mesh.n_points
+        assert torch.equal(packed[:n], wide[:n])
+
+
 def test_dense_wide_rows_and_layers_smoothing():
     """Dense iid volumes whose rows hold ~1400 points and whose layers hold ~600K points, so
     stencil neighbours are far apart in id space: extraction and smoothing still match the oracle."""
