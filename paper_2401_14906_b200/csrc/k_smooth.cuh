@@ -266,11 +266,13 @@ __device__ __forceinline__ uint2 nbr8_pack(uint32_t w, uint4 v, uint32_t f) {
     const uint32_t dmz = w - v.x, dmy = w - v.y, dpy = v.z - w, dpz = v.w - w;
     return make_uint2(dmz | (dpz << 21), (dpz >> 11) | (dmy << 10) | (dpy << 20) | (((f >> 2) & 3u) << 30));
 }
-__device__ __forceinline__ void nbr8_unpack(uint2 e, uint32_t w, uint32_t &f, uint4 &nb) {
-    const uint32_t dmz = e.x & 0x1FFFFFu, dpz = __funnelshift_r(e.x, e.y, 21) & 0x1FFFFFu;
-    const uint32_t dmy = (e.y >> 10) & 0x3FFu, dpy = (e.y >> 20) & 0x3FFu;
-    f = (dmz ? 1u : 0u) | (dmy ? 2u : 0u) | ((e.y >> 30) << 2) | (dpy ? 16u : 0u) | (dpz ? 32u : 0u);
-    nb = make_uint4(w - dmz, w - dmy, w + dpy, w + dpz);
+__device__ __forceinline__ uint32_t nbr8_faces(uint2 e) {
+    return ((e.x & 0x1FFFFFu) ? 1u : 0u) | ((e.y & (0x3FFu << 10)) ? 2u : 0u) | ((e.y >> 30) << 2) |
+           ((e.y & (0x3FFu << 20)) ? 16u : 0u) | ((__funnelshift_r(e.x, e.y, 21) & 0x1FFFFFu) ? 32u : 0u);
+}
+__device__ __forceinline__ uint4 nbr8_idx(uint2 e, uint32_t w) {
+    return make_uint4(w - (e.x & 0x1FFFFFu), w - ((e.y >> 10) & 0x3FFu), w + ((e.y >> 20) & 0x3FFu),
+                      w + (__funnelshift_r(e.x, e.y, 21) & 0x1FFFFFu));
 }
 
 __global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, const uint32_t *csr_off,
@@ -304,14 +306,15 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
         const uint32_t w = a.halo_lo + ii;
         uint32_t f;
         uint4 nb;
-        if (PACKED) {
-            nbr8_unpack(__ldg(a.nbr8 + ii), w, f, nb);
+        if constexpr (PACKED) {
+            const uint2 e = __ldg(a.nbr8 + ii);
+            f = act ? nbr8_faces(e) : 0u;
+            nb = nbr8_idx(e, w);
         } else {
             const uint4 nbw = __ldg(a.nbr + ii);
-            f = nbr_faces(nbw);
+            f = act ? nbr_faces(nbw) : 0u;
             nb = nbr_idx(nbw);
         }
-        if (!act) f = 0u;
         float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f), h0 = o4, h1 = o4, h2 = o4, h3 = o4;
         if (src) {
             o4 = __ldg(src + w);
