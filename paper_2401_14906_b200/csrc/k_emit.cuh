@@ -608,6 +608,14 @@ __global__ void __launch_bounds__(256) k_emit_row(EmitArgs a) {
 // memory.
 constexpr int kBand = 32;
 constexpr int kBandThreads = 256;
+#ifndef PSN_BAND_BUFS
+#define PSN_BAND_BUFS 2
+#endif
+constexpr int kBandBufs = PSN_BAND_BUFS;   // staged bands per CTA (ring; 2 keeps L1 for the label gathers)
+
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 constexpr uint32_t kStageCsr = 150;   // rounds with >= this many CSR ids write them through shared memory
 
 constexpr int kRangeCap = (kBand + 2) * 32 + 16;   // elements per staged range (+ alignment slack)
@@ -625,8 +633,10 @@ template <typename T, bool ANZ>
 __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
     constexpr int B = kBand;
     extern __shared__ __align__(128) uint8_t dsm_band[];
-    BandBuf *buf = reinterpret_cast<BandBuf *>(dsm_band);   // [2]
-    __shared__ __align__(8) uint64_t bar[2];
+    BandBuf *buf = reinterpret_cast<BandBuf *>(dsm_band);   // [kBandBufs]
+    __shared__ __align__(8) uint64_t bar[kBandBufs];
+    __shared__ int32_t s_band[kBandBufs];   // band staged in each buffer (nbands: end of the CTA's list)
+    __shared__ uint32_t s_done[kBandBufs];  // warps finished with each buffer
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
     __shared__ uint32_t scsr[kBandThreads / 32][6 * 32];   // a round's CSR ids, written out coalesced
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -635,7 +645,10 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
         for (int t = tid; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
         ls.bits = sbits;
     }
-    if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
+    if (tid == 0) {
+        for (int b = 0; b < kBandBufs; ++b) { mbar_init(&bar[b], 1); s_done[b] = 0u; }
+        fence_mbar_init();
+    }
     __syncthreads();
     const uint64_t totP = a.hdr->total[0], totQ = a.hdr->total[1], totS = a.hdr->total[2];
     const uint32_t halo_lo = (uint32_t)a.hdr->halo_lo;
@@ -716,10 +729,10 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
     };
 
     // Bands without points (outside the surfaces; most of a sparse volume) are skipped without
-    // staging: warp 0 looks 32 of the CTA's bands ahead at once (band b has points iff the
+    // staging: a warp looks 32 of the CTA's bands ahead at once (band b has points iff the
     // window offsets of its first and one-past-last rows differ) and stages the next non-empty one.
     const int32_t G = (int32_t)gridDim.x;
-    auto next_band = [&](int32_t c) -> int32_t {   // warp 0, all lanes; nbands if none
+    auto next_band = [&](int32_t c) -> int32_t {   // one full warp; nbands if none
         for (int32_t base = c; base < nbands; base += 32 * G) {
             const int32_t cand = base + lane * G;
             bool ne = false;
@@ -732,29 +745,52 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
         }
         return nbands;
     };
-    __shared__ int32_t s_nb[2];
+    // Stage list element `band` into buffer sb (lane 0): the band id rides with the fill (released
+    // by the arrive); an end marker is a fill without bytes.
+    auto stage = [&](int32_t band, int sb) {
+        s_band[sb] = band;
+        if (band < nbands) issue(band, sb);
+        else mbar_arrive_cta(&bar[sb]);
+    };
+    // Ring of kBandBufs staged bands, no CTA-wide barrier: a warp waits for the fill of its next
+    // buffer, emits its rows, and counts itself out of the buffer; the LAST warp out refills it
+    // with the band kBandBufs list elements ahead.  Fast warps run ahead by up to kBandBufs - 1
+    // bands instead of waiting at every band for the slowest warp (rows differ in point counts).
     if (warp == 0) {
-        const int32_t b0 = next_band(blockIdx.x);
-        if (lane == 0) {
-            s_nb[0] = b0;
-            if (b0 < nbands) issue(b0, 0);
+        int32_t b = blockIdx.x;
+        for (int i = 0; i < kBandBufs; ++i) {
+            b = next_band(b);
+            if (lane == 0) stage(b, i);
+            if (b < nbands) b += G;
         }
     }
-    uint32_t par[2] = {0u, 0u};
+    uint32_t par[kBandBufs];
+#pragma unroll
+    for (int i = 0; i < kBandBufs; ++i) par[i] = 0u;
     for (int it = 0;; ++it) {
-        __syncthreads();   // every thread is past the previous band (its buffer may be refilled) and s_nb is set
-        const int32_t band = s_nb[it & 1];
-        if (band >= nbands) break;
-        const int sb = it & 1;
-        if (warp == 0) {
-            const int32_t nb = next_band(band + G);
-            if (lane == 0) {
-                s_nb[sb ^ 1] = nb;
-                if (nb < nbands) issue(nb, sb ^ 1);
-            }
-        }
+        const int sb = it % kBandBufs;
         mbar_wait(&bar[sb], par[sb]);
         par[sb] ^= 1u;
+        const int32_t band = *reinterpret_cast<volatile int32_t *>(&s_band[sb]);
+        if (band >= nbands) break;
+        auto release = [&]() {   // this warp is done with buffer sb
+            __syncwarp();
+            uint32_t old = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                old = atomicAdd(&s_done[sb], 1u);
+            }
+            old = __shfl_sync(kFull, old, 0);
+            if (old == kBandThreads / 32 - 1) {   // last warp out: refill with the band kBandBufs ahead
+                __threadfence_block();
+                const int32_t prev = *reinterpret_cast<volatile int32_t *>(&s_band[(sb + kBandBufs - 1) % kBandBufs]);
+                const int32_t nb = prev < nbands ? next_band(prev + G) : nbands;
+                if (lane == 0) {
+                    s_done[sb] = 0u;
+                    stage(nb, sb);
+                }
+            }
+        };
         const BandBuf &bb = buf[sb];
         const int32_t rr0 = band * B;
         // staged-row accessors (element shifts of each range's aligned copy)
@@ -950,6 +986,7 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
             run_s += tot & 0xffffu;
             cur = nxt;
         }
+        release();
     }
 }
 

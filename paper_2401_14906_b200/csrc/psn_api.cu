@@ -216,8 +216,8 @@ cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int th
 template <typename T>
 void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st, int emit_mode) {
     if (fast && ea.W32 <= 32 && emit_mode == 0) {   // band-staged: shared-memory id lookups
-        if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, 2 * sizeof(BandBuf), st>>>(ea);
-        else k_emit_band<T, false><<<(unsigned)blocks, kBandThreads, 2 * sizeof(BandBuf), st>>>(ea);
+        if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
+        else k_emit_band<T, false><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
     } else if (fast && ea.W32 <= 32 && emit_mode == 1) {   // rows of <= 32 plane words: lane = word, metadata pipelined
         if (anz) k_emit_row<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
         else k_emit_row<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
@@ -455,10 +455,10 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
             for (const void *f : {(const void *)k_emit_band<uint8_t, true>, (const void *)k_emit_band<uint8_t, false>,
                                   (const void *)k_emit_band<uint16_t, true>, (const void *)k_emit_band<uint16_t, false>,
                                   (const void *)k_emit_band<uint32_t, true>, (const void *)k_emit_band<uint32_t, false>})
-                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sizeof(BandBuf)));
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBandBufs * sizeof(BandBuf)));
             attr = true;
         }
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBandThreads, 2 * sizeof(BandBuf));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBandThreads, kBandBufs * sizeof(BandBuf));
         blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + kBand - 1) / kBand, (int64_t)ctx->sms * std::max(occ, 1)));
     } else if (L.W32 <= 32) {   // k_emit_row: one resident wave of warps, each pipelining its rows
         int occ = 0;
