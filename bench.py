@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """bench.py -- PSN hot path on B200: extraction (k_count3 -> k_scan -> k_emit_band) +
-T-iteration constrained smoothing (k_smooth_prep + T x k_smooth_v4), timed with CUDA events.
+T-iteration constrained smoothing (k_smooth_prep8 + T x k_smooth_v4), timed with CUDA events.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl psn|reference]
 
@@ -307,7 +307,7 @@ def run_psn(args, rank, world, local_rank):
     sm_ptit = P * T / (t_sm * 1e-3)
     ext_gbs = b_ext / (t_ext * 1e-3) / 1e9
     # dominant kernel: k_smooth_v4 (T launches per step) -- achieved = B_sm per launch / avg launch time,
-    # the launch time taken as (psn_smooth time incl. the one-off k_smooth_prep) / T (conservative)
+    # the launch time taken as (psn_smooth time incl. the one-off k_smooth_prep8) / T (conservative)
     per_launch_ms = t_sm / max(T, 1)
     sm_gbs = b_sm / (per_launch_ms * 1e-3) / 1e9
     dominant = "k_smooth_v4" if t_sm >= t_ext else "extraction (k_count3+k_scan+k_emit_band)"
