@@ -161,8 +161,13 @@ psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh,
 psn_status psn_smooth_workspace(const psn_mesh *mesh, size_t *bytes);
 
 /* Build the smoothing cache of `mesh` into ws (psn_smooth does this itself;
- * slab users call it once before their psn_smooth_step loop). */
-psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_mesh *mesh, void *ws, size_t ws_bytes, void *stream);
+ * slab users call it once before their psn_smooth_step loop).  `vol` (dims)
+ * selects the cache form: the packed 8-byte one (id distances to the y/z
+ * neighbours) when M-1 < 2^10 and (M-1)(N-1) < 2^21 under the box
+ * constraint, else 16 bytes per point.  psn_smooth_step must be given the
+ * same volume.  PSN_ERR_ARG: NULL volume / mesh arrays, workspace too small. */
+psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, void *ws, size_t ws_bytes,
+                              void *stream);
 
 /*
  * Constrained Laplacian smoothing (Eq. 1) with double buffering
@@ -182,13 +187,17 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
 
 /*
  * One Jacobi iteration over the own points of a slab: reads the window offset
- * buffer src[n_window][3] (halo entries must hold the neighbours' current
- * values), writes the own entries of dst.  ws must hold the smoothing cache
- * built by psn_smooth_prepare.  src == NULL means "all offsets zero" (first
- * iteration from the anchors).
+ * buffer src[n_window][4] (float4 entries x, y, z, unused; 16-byte aligned;
+ * halo entries must hold the neighbours' current values), writes the own
+ * entries of dst (same layout; w written as 0).  ws must hold the smoothing
+ * cache built by psn_smooth_prepare for the same `vol`.  src == NULL means
+ * "all offsets zero" (first iteration from the anchors).  Same kernel and
+ * bits as psn_smooth's per-iteration path.  Box constraint only
+ * (PSN_ERR_ARG in sphere mode); PSN_ERR_ARG for NULL dst / vol, misaligned
+ * buffers or a workspace too small.
  */
-psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, const float *src,
-                           float *dst, float relaxation, float constraint_distance, void *stream);
+psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws, size_t ws_bytes,
+                           const float *src, float *dst, float relaxation, float constraint_distance, void *stream);
 
 /* Smoothing strategy of psn_smooth (whole volume):
  *   PSN_SMOOTH_PER_ITERATION (default): one launch per Jacobi iteration.
@@ -233,7 +242,8 @@ psn_status psn_ctx_set_emission(psn_ctx *ctx, int mode);
  * wavefront dependency wait timed out (a guard that must never trigger). */
 psn_status psn_smooth_status(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, void *stream);
 
-/* World coordinates of window entries [w0, w1) from offsets (NULL = anchors). */
+/* World coordinates out[w][3] of window entries [w0, w1) from float4 offsets
+ * offsets[n_window][4] as psn_smooth_step writes them (NULL = anchors). */
 psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
                                const float *offsets, int64_t w0, int64_t w1, float *out, void *stream);
 

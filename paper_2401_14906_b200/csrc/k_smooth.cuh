@@ -33,20 +33,6 @@ __device__ __forceinline__ uint32_t nbr_faces(uint4 v) {
     return (v.x >> 30) | ((v.y >> 30) << 2) | ((v.z >> 30) << 4);
 }
 
-struct SmoothArgs {
-    const float *src;          // window offsets [n_window][3]; NULL = all zero
-    float *dst;                // window offsets (own entries written)
-    float *world;              // if non-NULL: write world coordinates here instead of dst
-    const uint8_t *fmask;      // own points
-    const uint4 *nbr;          // own points: window indices of the -z,-y,+y,+z neighbours (k_smooth_prep)
-    const float *points;       // window anchors (fp32 voxel centres), for the world output
-    int64_t n_own;
-    uint32_t halo_lo;          // window index of the first own point
-    float lambda;
-    Constraint cons;
-    double sp[3], org[3];
-};
-
 __device__ __forceinline__ double anchor64_from(float p, double org, double sp) {
     const double idx = rint(__dsub_rn(__ddiv_rn(__dsub_rn((double)p, org), sp), 0.5));
     return __dadd_rn(org, __dmul_rn(__dadd_rn(idx, 0.5), sp));
@@ -162,87 +148,12 @@ __global__ void __launch_bounds__(256) k_smooth_prep(const uint8_t *fmask, const
     }
 }
 
-// One Jacobi step of Eq. 1 on index-space offsets (see header comment).
-// A warp owns 64 consecutive points (two per lane, lane and lane+32) so that
-// every load of both points is in flight before any is used.  The +-x
-// neighbours (w-1, w+1) come from the adjacent lanes by shuffle; the y/z
-// neighbours are gathered through the smoothing cache, unconditionally (absent
-// faces point at the point itself, a cache hit) and masked arithmetically.
-// sum_j (e_f + o_j - o_i) = e + sum_j o_j - deg * o_i.
-__device__ __forceinline__ float3 ld3(const float *__restrict__ p, uint32_t w) {
-    return make_float3(__ldg(p + 3u * w), __ldg(p + 3u * w + 1u), __ldg(p + 3u * w + 2u));
-}
-
-__global__ void __launch_bounds__(256) k_smooth(SmoothArgs a) {
-    const int lane = threadIdx.x & 31;
-    const float *__restrict__ src = a.src;
-    const uint32_t n = (uint32_t)a.n_own;
-    const uint32_t stride = gridDim.x * (blockDim.x >> 5) * 64u;
-    for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 64u; base < n; base += stride) {
-        uint32_t i[2], w[2], f[2];
-        uint4 nb[2];
-        float3 o[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            i[u] = base + 32u * u + lane;
-            const uint32_t ii = i[u] < n ? i[u] : n - 1u;
-            w[u] = a.halo_lo + ii;
-            f[u] = i[u] < n ? (uint32_t)__ldg(a.fmask + ii) : 0u;
-            nb[u] = nbr_idx(__ldg(a.nbr + ii));
-            o[u] = src ? ld3(src, w[u]) : make_float3(0.f, 0.f, 0.f);
-        }
-        // y/z gathers (all issued before the arithmetic)
-        float3 g[2][4];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (src) {
-                g[u][0] = ld3(src, nb[u].x); g[u][1] = ld3(src, nb[u].y);
-                g[u][2] = ld3(src, nb[u].z); g[u][3] = ld3(src, nb[u].w);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) g[u][q] = make_float3(0.f, 0.f, 0.f);
-            }
-        }
-        // +-x neighbours: lane-1 / lane+1 of the same half; across the halves and the warp ends
-        float3 mxo[2], pxo[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            mxo[u].x = __shfl_up_sync(kFull, o[u].x, 1); mxo[u].y = __shfl_up_sync(kFull, o[u].y, 1);
-            mxo[u].z = __shfl_up_sync(kFull, o[u].z, 1);
-            pxo[u].x = __shfl_down_sync(kFull, o[u].x, 1); pxo[u].y = __shfl_down_sync(kFull, o[u].y, 1);
-            pxo[u].z = __shfl_down_sync(kFull, o[u].z, 1);
-        }
-        {   // lane 31 of half 0 <-> lane 0 of half 1
-            const float bx = __shfl_sync(kFull, o[1].x, 0), by = __shfl_sync(kFull, o[1].y, 0), bz = __shfl_sync(kFull, o[1].z, 0);
-            const float ex = __shfl_sync(kFull, o[0].x, 31), ey = __shfl_sync(kFull, o[0].y, 31), ez = __shfl_sync(kFull, o[0].z, 31);
-            if (lane == 31) pxo[0] = make_float3(bx, by, bz);
-            if (lane == 0) mxo[1] = make_float3(ex, ey, ez);
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (i[u] >= n) continue;
-            const uint32_t fu = f[u];
-            if (fu && src) {
-                if ((fu & 4u) && lane == 0 && u == 0) mxo[0] = ld3(src, w[u] - 1u);
-                if ((fu & 8u) && (lane == 31 && u == 1 || i[u] + 1u >= n)) pxo[u] = ld3(src, w[u] + 1u);
-            }
-            const float3 r = jacobi_update(fu, o[u], mxo[u], pxo[u], g[u][0], g[u][1], g[u][2], g[u][3], a.lambda, a.cons);
-            const uint32_t ww = w[u];
-            if (a.world) {
-                a.world[3u * ww + 0u] = world_of(__ldg(a.points + 3u * ww + 0u), r.x, a.org[0], a.sp[0]);
-                a.world[3u * ww + 1u] = world_of(__ldg(a.points + 3u * ww + 1u), r.y, a.org[1], a.sp[1]);
-                a.world[3u * ww + 2u] = world_of(__ldg(a.points + 3u * ww + 2u), r.z, a.org[2], a.sp[2]);
-            } else {
-                a.dst[3u * ww + 0u] = r.x; a.dst[3u * ww + 1u] = r.y; a.dst[3u * ww + 2u] = r.z;
-            }
-        }
-    }
-}
-
 // One Jacobi step on float4 offsets (x, y, z, unused): one 16-byte load per
 // gathered neighbour instead of three scalar loads (the kernel is issue-bound,
 // not DRAM-bound, so the extra 4 bytes per point cost less than the saved
-// instructions).  Same arithmetic as k_smooth / k_smooth_tb (bit-identical).
+// instructions).  Same arithmetic as k_smooth_tb (bit-identical).  Used by
+// psn_smooth (whole volume, last step writes world coordinates) and by
+// psn_smooth_step (slabs / shards: one step between halo exchanges).
 struct SmoothV4 {
     const float4 *src;         // window offsets; NULL = all zero (first iteration)
     float4 *dst;
@@ -403,13 +314,14 @@ __global__ void __launch_bounds__(256) k_smooth_soa_sphere(SmoothSoASphere a) {
     }
 }
 
-// World coordinates of window entries [w0, w1) from offsets (NULL = anchors).
-__global__ void __launch_bounds__(256) k_finalize(const float *offs, const float *points, float *out,
+// World coordinates of window entries [w0, w1) from float4 offsets (NULL = anchors).
+__global__ void __launch_bounds__(256) k_finalize(const float4 *offs, const float *points, float *out,
                                                   int64_t w0, int64_t w1, double sx, double sy, double sz,
                                                   double ox, double oy, double oz) {
     for (int64_t w = w0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < w1;
          w += (int64_t)gridDim.x * blockDim.x) {
-        const float o0 = offs ? offs[3 * w] : 0.f, o1 = offs ? offs[3 * w + 1] : 0.f, o2 = offs ? offs[3 * w + 2] : 0.f;
+        const float4 o = offs ? offs[w] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float o0 = o.x, o1 = o.y, o2 = o.z;
         out[3 * w + 0] = world_of(points[3 * w + 0], o0, ox, sx);
         out[3 * w + 1] = world_of(points[3 * w + 1], o1, oy, sy);
         out[3 * w + 2] = world_of(points[3 * w + 2], o2, oz, sz);

@@ -544,19 +544,36 @@ Constraint make_constraint(int shape, float d, const double *sp) {
     return c;
 }
 
-SmoothArgs smooth_args(const psn_mesh *mesh, const void *ws, float lambda, float d) {
-    SmoothArgs a;
-    memset(&a, 0, sizeof(a));
-    a.fmask = mesh->face_masks;
-    a.nbr = static_cast<const uint4 *>(ws);
-    a.points = mesh->points; a.n_own = mesh->n_points;
-    a.halo_lo = (uint32_t)mesh->halo_lo_points;
-    a.lambda = lambda; a.cons = make_constraint(PSN_CONSTRAINT_BOX, d, nullptr);
-    return a;
-}
-
 int64_t grid_for(psn_ctx *ctx, int64_t n) {
     return std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 16));
+}
+
+// Packed 8-byte smoothing cache (k_smooth_prep8) for the box constraint when the volume's
+// rows / layers keep neighbour id distances within its fields: y < 2^10, z < 2^21.
+bool smooth_packed(const psn_ctx *ctx, const psn_volume *vol) {
+    if (!vol || ctx->constraint != PSN_CONSTRAINT_BOX || getenv("PSN_SMOOTH_NBR16")) return false;
+    const int64_t Mc = vol->dims[0] - 1, Nc = vol->dims[1] - 1;
+    return Mc < (1 << 10) && Mc * Nc < (1 << 21);
+}
+
+psn_status launch_prep8(psn_ctx *ctx, const psn_mesh *mesh, void *ws, cudaStream_t st) {
+    if (mesh->n_points == 0) return PSN_OK;
+    k_smooth_prep8<<<(unsigned)grid_for(ctx, mesh->n_points), 256, 0, st>>>(
+        mesh->face_masks, mesh->stencil_offsets, mesh->stencil_ids, static_cast<uint2 *>(ws), mesh->n_points,
+        (uint32_t)mesh->halo_lo_points, (uint32_t)(mesh->first_point - mesh->halo_lo_points),
+        (uint32_t)mesh->first_stencil);
+    ++ctx->launches;
+    return cuda_check(ctx, "smooth prep launch");
+}
+
+SmoothV4 smooth_v4_args(const psn_volume *vol, const psn_mesh *mesh, const void *ws, float lambda, float d) {
+    SmoothV4 v;
+    memset(&v, 0, sizeof(v));
+    v.nbr = static_cast<const uint4 *>(ws); v.nbr8 = static_cast<const uint2 *>(ws); v.points = mesh->points;
+    v.n_own = (uint32_t)mesh->n_points; v.halo_lo = (uint32_t)mesh->halo_lo_points;
+    v.lambda = lambda; v.d = d;
+    for (int c = 0; c < 3; ++c) { v.sp[c] = vol->spacing[c]; v.org[c] = vol->origin[c]; }
+    return v;
 }
 
 psn_status launch_prep(psn_ctx *ctx, const psn_mesh *mesh, void *ws, cudaStream_t st) {
@@ -570,14 +587,17 @@ psn_status launch_prep(psn_ctx *ctx, const psn_mesh *mesh, void *ws, cudaStream_
 }
 }  // namespace
 
-psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_mesh *mesh, void *ws, size_t ws_bytes, void *stream) {
+psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, void *ws, size_t ws_bytes,
+                              void *stream) {
     if (!ctx) return PSN_ERR_ARG;
     ctx->launches = 0;
     psn_status s = check_smooth_args(ctx, mesh, 0.f, 0.f);
     if (s != PSN_OK) return s;
+    if (!vol) return fail(ctx, PSN_ERR_ARG, "volume is NULL");
     if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
-    return launch_prep(ctx, mesh, ws, static_cast<cudaStream_t>(stream));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return smooth_packed(ctx, vol) ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st);
 }
 
 psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, float *out, int32_t iterations,
@@ -606,29 +626,12 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         return cuda_check(ctx, "finalize launch");
     }
     const Constraint cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
-    // packed 8-byte smoothing cache: y neighbours are < M ids away, z neighbours < (M-1)(N-1)
-    const int64_t Mc = vol->dims[0] - 1, Nc = vol->dims[1] - 1;
-    const bool packed = ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION && !cons.sphere && Mc < (1 << 10) &&
-                        Mc * Nc < (1 << 21) && !getenv("PSN_SMOOTH_NBR16");
-    if (packed) {
-        k_smooth_prep8<<<(unsigned)grid_for(ctx, nw), 256, 0, st>>>(
-            mesh->face_masks, mesh->stencil_offsets, mesh->stencil_ids, static_cast<uint2 *>(ws), nw,
-            (uint32_t)mesh->halo_lo_points, (uint32_t)(mesh->first_point - mesh->halo_lo_points),
-            (uint32_t)mesh->first_stencil);
-        ++ctx->launches;
-        if ((s = cuda_check(ctx, "smooth prep launch")) != PSN_OK) return s;
-    } else if ((s = launch_prep(ctx, mesh, ws, st)) != PSN_OK) {
-        return s;
-    }
+    const bool packed = ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION && smooth_packed(ctx, vol);
+    if ((s = packed ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
         // one launch per Jacobi iteration, offsets double-buffered in the two buffer slots
         if (!cons.sphere) {   // box constraint: float4 offsets (one 16-byte load per gather)
-            SmoothV4 v;
-            memset(&v, 0, sizeof(v));
-            v.nbr = static_cast<const uint4 *>(ws); v.nbr8 = static_cast<const uint2 *>(ws); v.points = mesh->points;
-            v.n_own = (uint32_t)mesh->n_points; v.halo_lo = (uint32_t)mesh->halo_lo_points;
-            v.lambda = relaxation; v.d = constraint_distance;
-            for (int c = 0; c < 3; ++c) { v.sp[c] = vol->spacing[c]; v.org[c] = vol->origin[c]; }
+            SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
             float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
             int occ4 = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, packed ? k_smooth_v4<true> : k_smooth_v4<false>, 256, 0);
@@ -745,22 +748,29 @@ psn_status psn_ctx_set_smoothing(psn_ctx *ctx, int mode, int32_t iterations_per_
     return PSN_OK;
 }
 
-psn_status psn_smooth_step(psn_ctx *ctx, const psn_mesh *mesh, const void *ws, size_t ws_bytes, const float *src,
-                           float *dst, float relaxation, float constraint_distance, void *stream) {
+psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws, size_t ws_bytes,
+                           const float *src, float *dst, float relaxation, float constraint_distance, void *stream) {
     if (!ctx) return PSN_ERR_ARG;
     ctx->launches = 0;
     psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
     if (s != PSN_OK) return s;
-    if (!dst) return fail(ctx, PSN_ERR_ARG, "dst is NULL");
+    if (!dst || !vol) return fail(ctx, PSN_ERR_ARG, "dst / volume is NULL");
     if (ctx->constraint != PSN_CONSTRAINT_BOX)
         return fail(ctx, PSN_ERR_ARG, "psn_smooth_step supports the box constraint (the sphere needs psn_smooth)");
     if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u)
+        return fail(ctx, PSN_ERR_ARG, "offset buffers must be 16-byte aligned (float4 entries)");
     if (mesh->n_points == 0) return PSN_OK;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
-    SmoothArgs a = smooth_args(mesh, ws, relaxation, constraint_distance);
-    a.src = src; a.dst = dst; a.world = nullptr;
-    const int64_t gs = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 511) / 512, (int64_t)ctx->sms * 16));
-    k_smooth<<<(unsigned)gs, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
+    v.src = reinterpret_cast<const float4 *>(src); v.dst = reinterpret_cast<float4 *>(dst); v.world = nullptr;
+    const bool packed = smooth_packed(ctx, vol);   // the form psn_smooth_prepare built for this volume
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, packed ? k_smooth_v4<true> : k_smooth_v4<false>, 256, 0);
+    const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (packed) k_smooth_v4<true><<<(unsigned)g4, 256, 0, st>>>(v);
+    else k_smooth_v4<false><<<(unsigned)g4, 256, 0, st>>>(v);
     ++ctx->launches;
     return cuda_check(ctx, "smooth step launch");
 }
@@ -773,9 +783,10 @@ psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_me
     const int64_t nw = mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points;
     if (w0 < 0 || w1 > nw || w0 > w1) return fail(ctx, PSN_ERR_ARG, "window range out of bounds");
     if (w0 == w1) return PSN_OK;
+    if (reinterpret_cast<uintptr_t>(offsets) & 15u) return fail(ctx, PSN_ERR_ARG, "offsets must be 16-byte aligned");
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     k_finalize<<<(unsigned)grid_for(ctx, w1 - w0), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        offsets, mesh->points, out, w0, w1, vol->spacing[0], vol->spacing[1], vol->spacing[2], vol->origin[0],
+        reinterpret_cast<const float4 *>(offsets), mesh->points, out, w0, w1, vol->spacing[0], vol->spacing[1], vol->spacing[2], vol->origin[0],
         vol->origin[1], vol->origin[2]);
     ++ctx->launches;
     return cuda_check(ctx, "finalize launch");

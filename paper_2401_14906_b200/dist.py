@@ -125,7 +125,7 @@ class SlabPipeline:
         self.plan = halo_plan(self.table, self.rank)
         nw = self.mesh.n_window
         self.sws = psn.smooth_workspace(self.mesh)
-        self.buf = [torch.zeros((max(nw, 1), 3), dtype=torch.float32, device=labels_slab.device) for _ in range(2)]
+        self.buf = [psn.offsets_buffer(nw, labels_slab.device) for _ in range(2)]   # float4 offsets
         self.out = torch.empty((max(nw, 1), 3), dtype=torch.float32, device=labels_slab.device)
 
     def extract(self, stream=None):
@@ -148,10 +148,10 @@ class SlabPipeline:
     def smooth(self, stream=None):
         """T Jacobi steps with a halo exchange after each (C2; the last one is C3)."""
         src = None
-        self.psn.smooth_prepare(self.mesh, self.sws, stream)
+        self.psn.smooth_prepare(self.vol, self.mesh, self.sws, stream)
         for t in range(self.T):
             dst = self.buf[t & 1]
-            self.psn.smooth_step(self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+            self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
             halo_exchange(dst, self.plan, self.rank, self.group)
             src = dst
         self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, 0, self.mesh.n_window, stream)
@@ -221,18 +221,18 @@ class BalancedSmoother:
         self.mesh = balance.shard_mesh(psn, self.shard)
         nw = max(self.shard.w1 - self.shard.w0, 1)
         self.sws = psn.smooth_workspace(self.mesh)
-        self.buf = [torch.zeros((nw, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.buf = [psn.offsets_buffer(nw, dev) for _ in range(2)]   # float4 offsets
         self.out = torch.empty((nw, 3), dtype=torch.float32, device=dev)
 
     def smooth(self, stream=None):
         sh = self.shard
         src = None
         if sh.n_points:
-            self.psn.smooth_prepare(self.mesh, self.sws, stream)
+            self.psn.smooth_prepare(self.vol, self.mesh, self.sws, stream)
         for t in range(self.T):
             dst = self.buf[t & 1]
             if sh.n_points:
-                self.psn.smooth_step(self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+                self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
             shard_halo_exchange(dst, self.windows, self.halo, self.rank, self.group)
             src = dst
         if sh.n_points:

@@ -87,13 +87,13 @@ def lib():
         L.psn_mesh_totals.restype = ctypes.c_int
         L.psn_smooth_workspace.argtypes = [ctypes.POINTER(MeshC), ctypes.POINTER(ctypes.c_size_t)]
         L.psn_smooth_workspace.restype = ctypes.c_int
-        L.psn_smooth_prepare.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
+        L.psn_smooth_prepare.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_smooth_prepare.restype = ctypes.c_int
         L.psn_smooth.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_int32,
                                  ctypes.c_float, ctypes.c_float, vp, ctypes.c_size_t, vp]
         L.psn_smooth.restype = ctypes.c_int
-        L.psn_smooth_step.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp, vp, ctypes.c_float,
-                                      ctypes.c_float, vp]
+        L.psn_smooth_step.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp, vp,
+                                      ctypes.c_float, ctypes.c_float, vp]
         L.psn_smooth_step.restype = ctypes.c_int
         L.psn_smooth_finalize.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, i64, i64, vp, vp]
         L.psn_smooth_finalize.restype = ctypes.c_int
@@ -330,13 +330,20 @@ class PSN:
     def smooth_status(self, mesh: Mesh, ws: torch.Tensor, stream=None):
         self._check(self.L.psn_smooth_status(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _stream(stream)))
 
-    def smooth_prepare(self, mesh: Mesh, ws: torch.Tensor, stream=None):
-        self._check(self.L.psn_smooth_prepare(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _stream(stream)))
+    def smooth_prepare(self, vol: Volume, mesh: Mesh, ws: torch.Tensor, stream=None):
+        self._check(self.L.psn_smooth_prepare(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(ws), ws.numel(),
+                                              _stream(stream)))
 
-    def smooth_step(self, mesh: Mesh, ws: torch.Tensor, src: torch.Tensor | None, dst: torch.Tensor,
+    @staticmethod
+    def offsets_buffer(n_window: int, device) -> torch.Tensor:
+        """A window offset buffer as psn_smooth_step reads / writes it: float32 [n_window][4]."""
+        return torch.zeros((max(n_window, 1), 4), dtype=torch.float32, device=device)
+
+    def smooth_step(self, vol: Volume, mesh: Mesh, ws: torch.Tensor, src: torch.Tensor | None, dst: torch.Tensor,
                     relaxation: float, constraint: float, stream=None):
-        rc = self.L.psn_smooth_step(self.h, ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _ptr(src), _ptr(dst),
-                                    float(relaxation), float(constraint), _stream(stream))
+        """One Jacobi step: src / dst are float32 [n_window][4] (x, y, z, unused) offset buffers."""
+        rc = self.L.psn_smooth_step(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _ptr(src),
+                                    _ptr(dst), float(relaxation), float(constraint), _stream(stream))
         self._check(rc)
 
     def smooth_finalize(self, vol: Volume, mesh: Mesh, offsets: torch.Tensor | None, out: torch.Tensor,

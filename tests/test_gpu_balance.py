@@ -50,14 +50,13 @@ def smooth_balanced(p, vols, meshes, firsts, total, G, T, lam, d):
     smeshes = [balance.shard_mesh(p, sh) for sh in shards]
     sws = [p.smooth_workspace(m) for m in smeshes]
     for m, w in zip(smeshes, sws):
-        p.smooth_prepare(m, w)
-    bufs = [[torch.zeros((max(sh.w1 - sh.w0, 1), 3), dtype=torch.float32, device="cuda") for _ in range(2)]
-            for sh in shards]
+        p.smooth_prepare(vols[0], m, w)
+    bufs = [[p.offsets_buffer(sh.w1 - sh.w0, "cuda") for _ in range(2)] for sh in shards]   # float4 offsets
     src = [None] * G
     for t in range(T):
         for r in range(G):
             if shards[r].n_points:
-                p.smooth_step(smeshes[r], sws[r], src[r], bufs[r][t & 1], lam, d)
+                p.smooth_step(vols[0], smeshes[r], sws[r], src[r], bufs[r][t & 1], lam, d)
         for (s, dd, g0, g1) in hm:   # halo exchange of the new windows
             bufs[dd][t & 1][g0 - shards[dd].w0:g1 - shards[dd].w0] = bufs[s][t & 1][g0 - shards[s].w0:g1 - shards[s].w0]
         src = [bufs[r][t & 1] for r in range(G)]

@@ -219,13 +219,20 @@ def test_degenerate_and_errors():
     try:
         p.set_constraint(1)
         ws = p.smooth_workspace(mesh)
-        p.smooth_prepare(mesh, ws)
-        dst = torch.empty_like(mesh.points)
+        p.smooth_prepare(vol, mesh, ws)
+        dst = p.offsets_buffer(mesh.n_window, "cuda")
         with pytest.raises(PSNError) as e:
-            p.smooth_step(mesh, ws, None, dst, 0.5, 0.5)
+            p.smooth_step(vol, mesh, ws, None, dst, 0.5, 0.5)
         assert e.value.status == PSN_ERR_ARG
     finally:
         p.set_constraint(0)
+    # float4 offset buffers must be 16-byte aligned
+    ws = p.smooth_workspace(mesh)
+    p.smooth_prepare(vol, mesh, ws)
+    flat = torch.zeros(4 * mesh.n_window + 1, dtype=torch.float32, device="cuda")
+    with pytest.raises(PSNError) as e:
+        p.smooth_step(vol, mesh, ws, None, flat[1:].view(-1, 4), 0.5, 0.5)
+    assert e.value.status == PSN_ERR_ARG
 
 
 def test_smoothing_zero_iterations_is_anchors():

@@ -36,15 +36,15 @@ def run_slabs(labels_np, G, T=6, lam=0.5, d=0.5, spacing=(1.0, 1.0, 1.0)):
         first = tuple(int(x) for x in table[:r, :3].sum(0)) if r else (0, 0, 0)
         meshes.append(p.emit(vols[r], p.labels(None), wss[r], counted[r], first=first))
     # smoothing with emulated halo exchange
-    bufs = [[torch.zeros((max(m.n_window, 1), 3), dtype=torch.float32, device="cuda") for _ in range(2)] for m in meshes]
+    bufs = [[p.offsets_buffer(m.n_window, "cuda") for _ in range(2)] for m in meshes]   # float4 offsets
     sws = [p.smooth_workspace(m) for m in meshes]
     for r in range(G):
-        p.smooth_prepare(meshes[r], sws[r])
+        p.smooth_prepare(vols[r], meshes[r], sws[r])
     plans = [halo_plan(table, r) for r in range(G)]
     src = [None] * G
     for t in range(T):
         for r in range(G):
-            p.smooth_step(meshes[r], sws[r], src[r], bufs[r][t & 1], lam, d)
+            p.smooth_step(vols[r], meshes[r], sws[r], src[r], bufs[r][t & 1], lam, d)
         for r in range(G):   # exchange: r's first layer -> r-1's upper halo, r's last layer -> r+1's lower halo
             dst = bufs[r][t & 1]
             if plans[r]["send_lo"] is not None:
