@@ -204,13 +204,18 @@ __global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, cons
     }
 }
 
-template <bool PACKED>
+template <bool PACKED, bool PREF = false>
 __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
     const float4 *__restrict__ src = a.src;
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint32_t base0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+    // PREF: the next grid-stride step's cache entry is loaded one step ahead, so only the
+    // neighbour gathers (not cache -> gathers) are on each step's critical path
+    uint2 e_next = make_uint2(0u, 0u);
+    if (PACKED && PREF && base0 < n) e_next = __ldg(a.nbr8 + min(base0 + lane, n - 1u));
+    for (uint32_t base = base0; base < n; base += stride) {
         const uint32_t i = base + lane;
         const bool act = i < n;
         const uint32_t ii = act ? i : n - 1u;
@@ -218,7 +223,13 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
         uint32_t f;
         uint4 nb;
         if constexpr (PACKED) {
-            const uint2 e = __ldg(a.nbr8 + ii);
+            uint2 e;
+            if constexpr (PREF) {
+                e = e_next;
+                if (base + stride < n) e_next = __ldg(a.nbr8 + min(base + stride + lane, n - 1u));
+            } else {
+                e = __ldg(a.nbr8 + ii);
+            }
             f = act ? nbr8_faces(e) : 0u;
             nb = nbr8_idx(e, w);
         } else {

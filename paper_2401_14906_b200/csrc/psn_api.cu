@@ -633,15 +633,19 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         if (!cons.sphere) {   // box constraint: float4 offsets (one 16-byte load per gather)
             SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
             float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
+            // one-step-ahead cache loads: measured faster up to tens of millions of points (c6
+            // -8 %, c4 -3 %) and slower on c5a's 133 M (+8 %), where the step is closest to
+            // the DRAM bound; chosen by size
+            void (*kern)(SmoothV4) = packed ? (nw < (1ll << 26) ? k_smooth_v4<true, true> : k_smooth_v4<true, false>)
+                                            : k_smooth_v4<false, false>;
             int occ4 = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, packed ? k_smooth_v4<true> : k_smooth_v4<false>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, kern, 256, 0);
             const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ4, 1)));
             const float4 *s4 = nullptr;
             for (int32_t t = 0; t < iterations; ++t) {
                 const bool last = (t == iterations - 1);
                 v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
-                if (packed) k_smooth_v4<true><<<(unsigned)g4, 256, 0, st>>>(v);
-                else k_smooth_v4<false><<<(unsigned)g4, 256, 0, st>>>(v);
+                kern<<<(unsigned)g4, 256, 0, st>>>(v);
                 ++ctx->launches;
                 s4 = v.dst;
             }
@@ -765,12 +769,12 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *
     SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
     v.src = reinterpret_cast<const float4 *>(src); v.dst = reinterpret_cast<float4 *>(dst); v.world = nullptr;
     const bool packed = smooth_packed(ctx, vol);   // the form psn_smooth_prepare built for this volume
+    void (*kern)(SmoothV4) = packed ? (mesh->n_points < (1ll << 26) ? k_smooth_v4<true, true> : k_smooth_v4<true, false>)
+                                    : k_smooth_v4<false, false>;
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, packed ? k_smooth_v4<true> : k_smooth_v4<false>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
     const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
-    const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (packed) k_smooth_v4<true><<<(unsigned)g4, 256, 0, st>>>(v);
-    else k_smooth_v4<false><<<(unsigned)g4, 256, 0, st>>>(v);
+    kern<<<(unsigned)g4, 256, 0, static_cast<cudaStream_t>(stream)>>>(v);
     ++ctx->launches;
     return cuda_check(ctx, "smooth step launch");
 }
