@@ -78,7 +78,7 @@ def halo_plan(table, rank: int):
 
 
 def halo_exchange(buf: torch.Tensor, plan, rank: int, group=None):
-    """C2/C3: send the boundary layers of `buf` ([n_window, 3]) and receive the halos.
+    """C2/C3: send the boundary layers of `buf` ([n_window, 4] float4 offsets) and receive the halos.
     NCCL point-to-point in one group (batch_isend_irecv)."""
     ops = []
     if plan["send_lo"] is not None:
