@@ -341,12 +341,12 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         ca.tma = ((L.M * eb) % 16 == 0) && ((reinterpret_cast<uintptr_t>(slab0) & 15u) == 0);
         cudaError_t ce;
         if (use3) {
-            // warp-per-row producer/consumer kernel: 8 voxel rows per CTA, z-chunks sized for
-            // ~8 waves of 2 CTAs per SM, each CTA marching >= 16 layers
+            // warp-per-row producer/consumer kernel: 16 voxel rows per CTA, z-chunks sized for
+            // ~8 waves of 2 CTAs per SM, each CTA marching >= 8 layers
             const int64_t nJB = (L.N - 1 + kC3Rows - 1) / kC3Rows;
             const int64_t target_ctas = (int64_t)ctx->sms * 2 * 8;
             int64_t nZC = std::max<int64_t>(1, (target_ctas + nJB - 1) / nJB);
-            nZC = std::min(nZC, std::max<int64_t>(1, nLay / 16));
+            nZC = std::min(nZC, std::max<int64_t>(1, nLay / 8));   // >= 8 layers per CTA (c2: 16 -> 8 is -10 %)
             nZC = std::min(nZC, nLay);
             const int64_t KZ = (nLay + nZC - 1) / nZC;
             nZC = (nLay + KZ - 1) / KZ;
