@@ -630,7 +630,7 @@ static_assert(sizeof(uint32_t) * kRangeCap % 16 == 0 && sizeof(uint16_t) * kRang
               "staged arrays must start at 16-byte boundaries");
 
 template <typename T, bool ANZ>
-__global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
+__global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
     constexpr int B = kBand;
     extern __shared__ __align__(128) uint8_t dsm_band[];
     BandBuf *buf = reinterpret_cast<BandBuf *>(dsm_band);   // [kBandBufs]
@@ -927,10 +927,30 @@ __global__ void __launch_bounds__(kBandThreads) k_emit_band(EmitArgs a) {
             const uint32_t tot = __shfl_sync(kFull, x, 31);
             const uint32_t ex = x - packed;
             const bool stage = (tot & 0xffffu) >= kStageCsr;   // dense round: CSR ids through shared memory
-            if (act) {
-                a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
-                a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
-                a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
+            if (!stage) {
+                if (act) {
+                    a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
+                    a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], j);
+                    a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], k);
+                }
+            } else {   // dense round (store-bound volumes): the round's points are ONE contiguous
+                // range of 3 * nact floats -- stage them in shared memory and write lane-contiguous
+                // words (full sectors instead of three 12-byte-strided stores per lane)
+                float *sp = reinterpret_cast<float *>(scsr[warp]);
+                if (act) {
+                    sp[3 * lane + 0] = anchor_coord(a.org[0], a.sp[0], i);
+                    sp[3 * lane + 1] = anchor_coord(a.org[1], a.sp[1], j);
+                    sp[3 * lane + 2] = anchor_coord(a.org[2], a.sp[2], k);
+                }
+                __syncwarp();
+                const uint32_t nact = __popc(__ballot_sync(kFull, act));
+                float *dstp = a.points + 3 * (size_t)(offP0 + cur.base);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const uint32_t e = (uint32_t)lane + 32u * q;
+                    if (e < 3u * nact) dstp[e] = sp[e];
+                }
+                __syncwarp();
             }
             if (own) {
                 const uint32_t wl = (uint32_t)i >> 5, below = (1u << (i & 31)) - 1u;
