@@ -6,7 +6,9 @@ T-iteration constrained smoothing (k_smooth_prep8 + T x k_smooth_v4), timed with
 
 N > 1 is launched by torchrun (one process per GPU, NCCL): the c4 volume is
 z-slab partitioned (strong scaling, total work fixed), with the all-gather of
-per-rank totals (C1) and the per-iteration halo exchange (C2).
+per-rank totals (C1), the point-balanced re-cut of the smoothing (C4) and the
+per-iteration halo exchange (C2), fused into the smoothing kernel as NVLink
+peer pushes (--nccl-halo: NCCL point-to-point instead).
 
 One JSON line on rank 0.  `value` = label voxels of the whole volume pushed
 through one step (extraction + T smoothing iterations) per second; the
@@ -246,7 +248,9 @@ def run_psn(args, rank, world, local_rank):
         k0, k1 = partition(O - 1, world)[rank]
         z_lo, z_hi = slab_slices(O, k0, k1)
         labels = psn_gen.generate_device(spec, z_lo, z_hi)
-        pipe = SlabPipeline(psn, labels, (M, N, O), sp, (0.0, 0.0, 0.0), (k0, k1), T, lam, d)
+        # C2 fused into the smoothing kernel (peer pushes over NVLink) unless --nccl-halo
+        pipe = SlabPipeline(psn, labels, (M, N, O), sp, (0.0, 0.0, 0.0), (k0, k1), T, lam, d,
+                            peer=not args.nccl_halo)
         tab = pipe.table
         P, Q, S = (int(x) for x in tab[:, :3].sum(0))
         run_extract = pipe.extract
@@ -267,6 +271,10 @@ def run_psn(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world == 1:
         assert pipe.check(), "steady-state totals differ from the warm-up count"
+    halo_peer = False
+    if world > 1:
+        ph = pipe.peer_halo if args.no_balance else pipe.balanced.peer
+        halo_peer = ph is not None
     launches = 0
     if world == 1:
         launches = sum(pipe.launches.values())
@@ -299,6 +307,8 @@ def run_psn(args, rank, world, local_rank):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ext, t_sm, t_step = (float(x) for x in tt.tolist())
     clocks = clk.summary()
+    if world > 1 and halo_peer:
+        (pipe.peer_halo if args.no_balance else pipe.balanced.peer).check()   # no peer wait timed out
 
     peak, peak_src = measured_peaks()
     b_ext, b_sm = algorithmic_bytes(V, b, P, Q, S)
@@ -368,7 +378,9 @@ def run_psn(args, rank, world, local_rank):
             "dtype": {1: "u8", 2: "u16", 4: "u32"}[b] + "/f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[cfg], "dims": [M, N, O], "label_bytes": b, "iterations": T,
                        "relaxation": lam, "constraint_voxels": d, "spacing": list(sp),
-                       "parallelism": (f"z-slab x{world}" + ("" if args.no_balance else ", point-balanced smoothing"))
+                       "parallelism": (f"z-slab x{world}" + ("" if args.no_balance else ", point-balanced smoothing")
+                                       + (", halo: kernel peer pushes (NVLink, CUDA IPC)" if halo_peer
+                                          else ", halo: NCCL point-to-point"))
                        if world > 1 else "single GPU",
                        "l2": ("inputs larger than L2 (%.2f GB labels, %.2f GB smoothing state)" % (V * b / 1e9, P * 28 / 1e9))
                        if V * b > l2 else "inputs fit in L2 (no flush; absolute numbers only)"},
@@ -394,6 +406,8 @@ def main():
     ap.add_argument("--impl", default="psn", choices=["psn", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-balance", action="store_true", help="N > 1: smooth on the extraction slabs (no C4 re-cut)")
+    ap.add_argument("--nccl-halo", action="store_true",
+                    help="N > 1: smoothing halo exchange over NCCL point-to-point instead of the kernel's peer pushes")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-voxels", type=float, default=96e6, help="oracle sample size for cpu_baseline (~10-30 s)")

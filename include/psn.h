@@ -258,6 +258,56 @@ psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *poin
 /* Number of kernel launches the last call on this ctx enqueued (bench.py's gpu_launches). */
 int64_t psn_launch_count(const psn_ctx *ctx);
 
+/* ------------------------------------------------------------------------
+ * Peer (NVLink) halo exchange for the slab / shard smoothing loop (SURVEY
+ * 8(e) v2; sub-volumes with open boundaries exchange the
+ * boundary layer every Jacobi step).  Instead of a collective after each
+ * psn_smooth_step, psn_smooth_step_peer's kernel stores the boundary layers
+ * it computes straight into the neighbours' offset buffers (peer pointers,
+ * CUDA IPC over NVLink) and signals them; a step starts once both neighbours
+ * have finished the previous one.  One launch per iteration, no host sync.
+ * ------------------------------------------------------------------------ */
+
+/* CUDA IPC handle of the device allocation holding `dev_ptr` (+ the offset of
+ * dev_ptr inside it), to be sent to the peer processes (host bytes).
+ * PSN_ERR_CUDA if the memory cannot be exported (e.g. not from cudaMalloc). */
+typedef struct { unsigned char handle[64]; uint64_t offset; } psn_ipc_handle;
+psn_status psn_ipc_export(psn_ctx *ctx, const void *dev_ptr, psn_ipc_handle *out);
+/* Map a peer process's exported allocation into this process (peer access
+ * enabled for the context's device); *dev_ptr = mapped base + offset.
+ * Release with psn_ipc_close(mapped pointer). */
+psn_status psn_ipc_open(psn_ctx *ctx, const psn_ipc_handle *h, void **dev_ptr);
+psn_status psn_ipc_close(psn_ctx *ctx, void *dev_ptr);
+
+typedef struct {
+    float *dst[2];              /* the neighbour's float4 [W'][4] offset buffers by parity (peer
+                                   pointers); dst[0] == NULL: no neighbour on this side */
+    int64_t src_begin, src_end; /* own window entries pushed (inside the own range) */
+    int64_t dst_begin;          /* the neighbour's window index receiving src_begin */
+    uint64_t *peer_sig;         /* the neighbour's signal word for this rank's pushes */
+} psn_peer_side;
+
+typedef struct {
+    psn_peer_side side[2];      /* [0] = lower neighbour (rank - 1), [1] = upper (rank + 1) */
+    uint64_t *sig;              /* this rank's signal words [2] (device; [0] written by the lower,
+                                   [1] by the upper neighbour; zeroed once before the first step) */
+    uint64_t *ctr;              /* this rank's CTA completion counter (device, zeroed once) */
+    uint32_t *err;              /* timeout flag (device, zeroed once): a wait > 5 s sets it */
+    uint64_t ctr_base;          /* in/out: CTAs counted on ctr so far (advanced by each call) */
+    uint64_t iteration;         /* in/out: global iteration index (advanced by each call) */
+} psn_peer;
+
+/* psn_smooth_step plus the peer push: writes dst (own entries) and, for own
+ * window entries [side.src_begin, side.src_end), the neighbour's buffer
+ * side.dst[parity] at side.dst_begin + (w - src_begin).  Every rank calls it
+ * once per iteration with the same `parity` (the caller's dst buffer index).
+ * Ranks without points still call it (the step only waits and signals).
+ * PSN_ERR_ARG for the conditions of psn_smooth_step, a NULL peer / sig / ctr /
+ * err, or a push range outside the own entries. */
+psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
+                                size_t ws_bytes, const float *src, float *dst, int parity, float relaxation,
+                                float constraint_distance, psn_peer *peer, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

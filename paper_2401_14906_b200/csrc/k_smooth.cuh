@@ -154,6 +154,29 @@ __global__ void __launch_bounds__(256) k_smooth_prep(const uint8_t *fmask, const
 // instructions).  Same arithmetic as k_smooth_tb (bit-identical).  Used by
 // psn_smooth (whole volume, last step writes world coordinates) and by
 // psn_smooth_step (slabs / shards: one step between halo exchanges).
+// Peer (NVLink) halo push of one slab / shard step (SV 8(e) v2; psn_smooth_step_peer).
+// side[0] = the lower neighbour (rank - 1), side[1] = the upper one (rank + 1).  Own
+// window entries [src_begin, src_end) are ALSO stored into the neighbour's offset
+// buffer `dst` (a peer pointer) at its window index dst_begin + (w - src_begin).
+// Iteration g of every rank starts when both neighbours have finished g - 1
+// (their signal words in this rank's memory, sig[0] from below, sig[1] from above,
+// hold >= g) and ends, after every CTA has fenced its stores system-wide, with the
+// last CTA writing g + 1 into the neighbours' signal words (release, system scope).
+struct PeerSide {
+    float4 *dst;               // the neighbour's buffer of this iteration's parity; NULL = no neighbour
+    uint32_t src_begin, src_end, dst_begin;
+    uint64_t *peer_sig;        // the neighbour's signal word for data from this rank
+};
+struct PeerArgs {
+    PeerSide side[2];
+    const uint64_t *sig;       // this rank's signal words [2] (written by the neighbours)
+    unsigned long long *ctr;   // this rank's CTA completion counter (monotonic)
+    unsigned long long ctr_last;   // counter value seen by the last CTA of this launch
+    uint32_t *err;             // set on a wait timeout (a guard that must never trigger)
+    uint64_t g;                // global iteration index of this step
+};
+constexpr uint64_t kPeerTimeoutNs = 5000000000ull;   // 5 s
+
 struct SmoothV4 {
     const float4 *src;         // window offsets; NULL = all zero (first iteration)
     float4 *dst;
@@ -164,6 +187,7 @@ struct SmoothV4 {
     uint32_t n_own, halo_lo;
     float lambda, d;
     double sp[3], org[3];
+    PeerArgs peer;             // used by k_smooth_v4<..., PEER = true> only
 };
 
 // Packed smoothing cache, 8 bytes per point (k_smooth_prep8): the id DISTANCES
@@ -204,10 +228,23 @@ __global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, cons
     }
 }
 
-template <bool PACKED, bool PREF = false>
+template <bool PACKED, bool PREF = false, bool PEER = false>
 __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
+    if constexpr (PEER) {   // both neighbours finished iteration g - 1 (their halo pushes are here)
+        if (threadIdx.x == 0) {
+            const uint64_t t0 = globaltimer_ns();
+            for (int s = 0; s < 2; ++s) {
+                if (!a.peer.side[s].dst) continue;
+                while (ld_acquire_sys64(a.peer.sig + s) < a.peer.g) {
+                    if (globaltimer_ns() - t0 > kPeerTimeoutNs) { atomicExch(a.peer.err, 1u); break; }
+                    __nanosleep(64);
+                }
+            }
+        }
+        __syncthreads();
+    }
     const float4 *__restrict__ src = a.src;
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t base0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -258,7 +295,27 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
             a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
             a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
         } else {
-            a.dst[w] = make_float4(r.x, r.y, r.z, 0.f);
+            const float4 r4 = make_float4(r.x, r.y, r.z, 0.f);
+            a.dst[w] = r4;
+            if constexpr (PEER) {   // boundary layers also go straight into the neighbours' halos
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const PeerSide &ps = a.peer.side[s];
+                    if (ps.dst && w >= ps.src_begin && w < ps.src_end) ps.dst[ps.dst_begin + (w - ps.src_begin)] = r4;
+                }
+            }
+        }
+    }
+    if constexpr (PEER) {   // this CTA's stores (local and peer) are visible system-wide; the last CTA signals
+        __threadfence_system();   // every thread fences its own stores
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long old = atomicAdd(a.peer.ctr, 1ull);
+            if (old == a.peer.ctr_last) {
+                __threadfence_system();
+                for (int s = 0; s < 2; ++s)
+                    if (a.peer.side[s].dst) st_release_sys64(a.peer.side[s].peer_sig, a.peer.g + 1);
+            }
         }
     }
 }

@@ -43,6 +43,7 @@ struct psn_ctx {
     int count_mode = PSN_COUNT_AUTO;          // psn_ctx_set_counting
     int emit_mode = PSN_EMIT_AUTO;            // psn_ctx_set_emission
     int constraint = PSN_CONSTRAINT_BOX;      // psn_ctx_set_constraint
+    std::map<void *, void *> ipc_bases;       // psn_ipc_open: returned pointer -> mapped base
 };
 
 namespace {
@@ -777,6 +778,104 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *
     kern<<<(unsigned)g4, 256, 0, static_cast<cudaStream_t>(stream)>>>(v);
     ++ctx->launches;
     return cuda_check(ctx, "smooth step launch");
+}
+
+psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
+                                size_t ws_bytes, const float *src, float *dst, int parity, float relaxation,
+                                float constraint_distance, psn_peer *peer, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
+    if (s != PSN_OK) return s;
+    if (!dst || !vol || !peer || !peer->sig || !peer->ctr || !peer->err)
+        return fail(ctx, PSN_ERR_ARG, "dst / volume / peer descriptor is NULL");
+    if (parity != 0 && parity != 1) return fail(ctx, PSN_ERR_ARG, "parity must be 0 or 1");
+    if (ctx->constraint != PSN_CONSTRAINT_BOX)
+        return fail(ctx, PSN_ERR_ARG, "psn_smooth_step_peer supports the box constraint");
+    if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u)
+        return fail(ctx, PSN_ERR_ARG, "offset buffers must be 16-byte aligned (float4 entries)");
+    const int64_t own0 = mesh->halo_lo_points, own1 = own0 + mesh->n_points;
+    SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
+    v.src = reinterpret_cast<const float4 *>(src); v.dst = reinterpret_cast<float4 *>(dst); v.world = nullptr;
+    for (int k = 0; k < 2; ++k) {
+        const psn_peer_side &ps = peer->side[k];
+        PeerSide &o = v.peer.side[k];
+        if (!ps.dst[0]) continue;
+        if (!ps.dst[1] || !ps.peer_sig || ps.src_begin < own0 || ps.src_end > own1 || ps.src_begin > ps.src_end ||
+            ps.dst_begin < 0 || ((reinterpret_cast<uintptr_t>(ps.dst[parity])) & 15u))
+            return fail(ctx, PSN_ERR_ARG, "peer side %d: bad buffers or push range", k);
+        o.dst = reinterpret_cast<float4 *>(ps.dst[parity]);
+        o.src_begin = (uint32_t)ps.src_begin; o.src_end = (uint32_t)ps.src_end; o.dst_begin = (uint32_t)ps.dst_begin;
+        o.peer_sig = ps.peer_sig;
+    }
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    const bool packed = smooth_packed(ctx, vol);
+    void (*kern)(SmoothV4) = packed ? k_smooth_v4<true, false, true> : k_smooth_v4<false, false, true>;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+    const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
+    v.peer.sig = peer->sig; v.peer.ctr = reinterpret_cast<unsigned long long *>(peer->ctr); v.peer.err = peer->err;
+    v.peer.ctr_last = (unsigned long long)(peer->ctr_base + (uint64_t)g4 - 1);
+    v.peer.g = peer->iteration;
+    kern<<<(unsigned)g4, 256, 0, static_cast<cudaStream_t>(stream)>>>(v);
+    ++ctx->launches;
+    if ((s = cuda_check(ctx, "smooth step (peer) launch")) != PSN_OK) return s;
+    peer->ctr_base += (uint64_t)g4;
+    peer->iteration += 1;
+    return PSN_OK;
+}
+
+psn_status psn_ipc_export(psn_ctx *ctx, const void *dev_ptr, psn_ipc_handle *out) {
+    if (!ctx) return PSN_ERR_ARG;
+    if (!dev_ptr || !out) return fail(ctx, PSN_ERR_ARG, "NULL argument");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    // base of the cudaMalloc allocation holding dev_ptr (driver entry point, no libcuda link)
+    typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(ctx, PSN_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+        get_range = reinterpret_cast<GetRange>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+        return fail(ctx, PSN_ERR_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, reinterpret_cast<void *>((uintptr_t)base)) != cudaSuccess)
+        return cuda_check(ctx, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) <= sizeof(out->handle), "IPC handle size");
+    memset(out, 0, sizeof(*out));
+    memcpy(out->handle, &h, sizeof(h));
+    out->offset = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+    return PSN_OK;
+}
+
+psn_status psn_ipc_open(psn_ctx *ctx, const psn_ipc_handle *hh, void **dev_ptr) {
+    if (!ctx) return PSN_ERR_ARG;
+    if (!hh || !dev_ptr) return fail(ctx, PSN_ERR_ARG, "NULL argument");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hh->handle, sizeof(h));
+    void *base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return cuda_check(ctx, "cudaIpcOpenMemHandle");
+    *dev_ptr = static_cast<char *>(base) + hh->offset;
+    ctx->ipc_bases[*dev_ptr] = base;
+    return PSN_OK;
+}
+
+psn_status psn_ipc_close(psn_ctx *ctx, void *dev_ptr) {
+    if (!ctx) return PSN_ERR_ARG;
+    auto it = ctx->ipc_bases.find(dev_ptr);
+    if (it == ctx->ipc_bases.end()) return fail(ctx, PSN_ERR_ARG, "pointer was not opened by psn_ipc_open");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    const cudaError_t e = cudaIpcCloseMemHandle(it->second);
+    ctx->ipc_bases.erase(it);
+    return e == cudaSuccess ? PSN_OK : cuda_check(ctx, "cudaIpcCloseMemHandle");
 }
 
 psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const float *offsets,

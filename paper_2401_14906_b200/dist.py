@@ -19,6 +19,15 @@ interior side).  The path has two real exchange steps:
       the moved points' face masks / CSR rows / anchors sent point-to-point to
       their new owners; C2 then runs on the re-cut windows.
 
+  C2 v2 (peer=True, SV 8(e) v2): the halo exchange is fused into the smoothing
+      kernel -- psn_smooth_step_peer stores the boundary layers it computes
+      straight into the neighbours' offset buffers over NVLink (CUDA IPC peer
+      pointers, exchanged once) and signals them; a step starts once both
+      neighbours finished the previous one.  No collective and no host sync
+      in the iteration loop.  Used when every halo move is between adjacent
+      ranks (always for slabs; for balanced shards in practice), else C2 over
+      NCCL.
+
 The collectives use torch.distributed (NCCL on GPUs; gloo in the CPU tests).
 """
 from __future__ import annotations
@@ -100,6 +109,106 @@ def halo_exchange(buf: torch.Tensor, plan, rank: int, group=None):
             r.wait()
 
 
+def peer_sides(rank: int, world: int, sends):
+    """Symmetric peer-push plan for psn_smooth_step_peer.
+
+    sends: [(src, dst, src_begin, src_end, dst_begin)] -- every rank's pushes,
+    window index ranges in src's window and the receiving index in dst's window
+    (the same list on all ranks).  Returns (lower, upper) for `rank`: None if
+    there is no exchange with that neighbour, else (src_begin, src_end,
+    dst_begin) of this rank's push to it (an empty range when only the
+    neighbour pushes here -- the signal still has to flow both ways, because a
+    rank may only push into a neighbour that has finished the previous step).
+    Raises ValueError if a push is not between adjacent ranks or a rank pushes
+    two ranges to one neighbour (the caller then falls back to NCCL)."""
+    out = {}
+    touch = set()
+    for (sr, dr, a, b, c) in sends:
+        if b <= a:
+            continue
+        if abs(sr - dr) != 1:
+            raise ValueError(f"push {sr}->{dr} is not between adjacent ranks")
+        if (sr, dr) in out:
+            raise ValueError(f"rank {sr} pushes two ranges to {dr}")
+        out[(sr, dr)] = (a, b, c)
+        touch.add((min(sr, dr), max(sr, dr)))
+    res = []
+    for nb in (rank - 1, rank + 1):
+        if nb < 0 or nb >= world or (min(rank, nb), max(rank, nb)) not in touch:
+            res.append(None)
+            continue
+        res.append(out.get((rank, nb), (0, 0, 0)))
+    return res[0], res[1]
+
+
+def slab_sends(table):
+    """Peer pushes of the z-slab halo plan: rank r's first own layer -> rank r-1's
+    upper halo, its last own layer -> rank r+1's lower halo."""
+    world = table.shape[0]
+    sends = []
+    for r in range(world):
+        pl = halo_plan(table, r)
+        if pl["send_lo"] is not None:
+            a, b = pl["send_lo"]
+            c, _ = halo_plan(table, r - 1)["recv_hi"]
+            sends.append((r, r - 1, a, b, c))
+        if pl["send_hi"] is not None:
+            a, b = pl["send_hi"]
+            c, _ = halo_plan(table, r + 1)["recv_lo"]
+            sends.append((r, r + 1, a, b, c))
+    return sends
+
+
+def shard_sends(halo, windows):
+    """Peer pushes of the balanced shards: halo move (src, dst, g0, g1) of global ids
+    -> (src, dst, g0 - w0[src], g1 - w0[src], g0 - w0[dst])."""
+    return [(s_, d_, g0 - windows[s_][0], g1 - windows[s_][0], g0 - windows[d_][0]) for (s_, d_, g0, g1) in halo]
+
+
+class PeerHalo:
+    """The peer-push state of one rank (psn_smooth_step_peer): its two float4
+    offset buffers and signal words exported once over CUDA IPC, the
+    neighbours' mapped, and the psn_peer descriptor advanced by every step."""
+
+    def __init__(self, psn, bufs, lower, upper, group=None):
+        from .psn import Peer
+        self.psn, self.bufs = psn, bufs
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        dev = bufs[0].device
+        self.sig = torch.zeros(2, dtype=torch.int64, device=dev)     # u64 words, written by the neighbours
+        self.ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)   # zeroed before any neighbour can signal
+        mine = [psn.ipc_export(bufs[0]), psn.ipc_export(bufs[1]), psn.ipc_export(self.sig)]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.peer = Peer()
+        self.peer.sig, self.peer.ctr, self.peer.err = self.sig.data_ptr(), self.ctr.data_ptr(), self.err.data_ptr()
+        self.opened = []
+        for k, (nb, spec) in enumerate(((rank - 1, lower), (rank + 1, upper))):
+            if spec is None:
+                continue
+            b0, b1, sg = (psn.ipc_open(h) for h in allh[nb])
+            self.opened += [b0, b1, sg]
+            side = self.peer.side[k]
+            side.dst[0], side.dst[1] = b0, b1
+            side.src_begin, side.src_end, side.dst_begin = spec
+            side.peer_sig = sg + 8 * (1 - k)   # pushes down land in the lower rank's sig[1], up in sig[0]
+        dist.barrier(group=group)   # every rank mapped its neighbours before anyone signals
+
+    def step(self, vol, mesh, ws, src, dst, parity, lam, d, stream=None):
+        self.psn.smooth_step_peer(vol, mesh, ws, src, dst, parity, lam, d, self.peer, stream)
+
+    def check(self):
+        if int(self.err.item()):
+            raise RuntimeError("peer halo wait timed out (a neighbour stopped stepping)")
+
+    def close(self):
+        for a in self.opened:
+            self.psn.ipc_close(a)
+        self.opened = []
+
+
 class SlabPipeline:
     """One rank's slab: extraction with halos + smoothing with halo exchange.
 
@@ -107,9 +216,10 @@ class SlabPipeline:
     the same psn_extract / psn_smooth_step calls)."""
 
     def __init__(self, psn, labels_slab: torch.Tensor, dims, spacing, origin, own, iterations, relaxation,
-                 constraint, label_set=None, group=None):
+                 constraint, label_set=None, group=None, peer: bool = False):
         from .psn import MeshC
-        self.psn, self.group = psn, group
+        self.psn, self.group, self.use_peer = psn, group, peer
+        self.peer_halo, self._shard_cache = None, {}
         self.rank = dist.get_rank(group)
         z_lo = slab_slices(dims[2], own[0], own[1])[0]
         self.vol = psn.volume(labels_slab, dims=dims, spacing=spacing, origin=origin, z_lo=z_lo, own=own)
@@ -142,17 +252,29 @@ class SlabPipeline:
         global smoothed points (ids [cuts[rank], cuts[rank+1]))."""
         total = int(self.table[:, 0].sum())
         self.balanced = BalancedSmoother(self.psn, self.vol, self.mesh, self.first_point, self.first_stencil, total,
-                                         self.T, self.lam, self.d, self.group)
+                                         self.T, self.lam, self.d, self.group, peer=self.use_peer,
+                                         cache=self._shard_cache)
         return self.balanced.smooth(stream)
 
     def smooth(self, stream=None):
-        """T Jacobi steps with a halo exchange after each (C2; the last one is C3)."""
+        """T Jacobi steps with a halo exchange after each (C2; the last one is C3):
+        fused into the step kernel (peer pushes) when peer=True, else NCCL."""
         src = None
         self.psn.smooth_prepare(self.vol, self.mesh, self.sws, stream)
+        if self.use_peer:
+            key = self.table.numpy().tobytes()   # halo sizes follow this step's per-rank counts
+            if self.peer_halo is None or self._peer_key != key:
+                if self.peer_halo is not None:
+                    self.peer_halo.close()
+                lower, upper = peer_sides(self.rank, dist.get_world_size(self.group), slab_sends(self.table))
+                self.peer_halo, self._peer_key = PeerHalo(self.psn, self.buf, lower, upper, self.group), key
         for t in range(self.T):
             dst = self.buf[t & 1]
-            self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
-            halo_exchange(dst, self.plan, self.rank, self.group)
+            if self.use_peer:
+                self.peer_halo.step(self.vol, self.mesh, self.sws, src, dst, t & 1, self.lam, self.d, stream)
+            else:
+                self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+                halo_exchange(dst, self.plan, self.rank, self.group)
             src = dst
         self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, 0, self.mesh.n_window, stream)
         return self.out
@@ -200,7 +322,7 @@ class BalancedSmoother:
     world coordinates of this rank's own ids [cuts[rank], cuts[rank+1])."""
 
     def __init__(self, psn, vol, mesh, first_point: int, first_stencil: int, total_points: int, iterations: int,
-                 relaxation: float, constraint: float, group=None):
+                 relaxation: float, constraint: float, group=None, peer: bool = False, cache=None):
         self.psn, self.vol, self.group = psn, vol, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.T, self.lam, self.d = iterations, relaxation, constraint
@@ -221,7 +343,24 @@ class BalancedSmoother:
         self.mesh = balance.shard_mesh(psn, self.shard)
         nw = max(self.shard.w1 - self.shard.w0, 1)
         self.sws = psn.smooth_workspace(self.mesh)
-        self.buf = [psn.offsets_buffer(nw, dev) for _ in range(2)]   # float4 offsets
+        self.peer = None
+        key = (tuple(self.cuts), tuple(self.windows))
+        if cache is not None and key in cache:   # same shard layout as an earlier step: reuse buffers + IPC maps
+            self.buf, self.peer = cache[key]
+        else:
+            self.buf = [psn.offsets_buffer(nw, dev) for _ in range(2)]   # float4 offsets
+            if peer:
+                try:
+                    lower, upper = peer_sides(self.rank, self.world, shard_sends(self.halo, self.windows))
+                    self.peer = PeerHalo(psn, self.buf, lower, upper, group)
+                except ValueError:
+                    self.peer = None   # a non-adjacent halo move: C2 over NCCL
+            if cache is not None:
+                for (_, old_peer) in cache.values():
+                    if old_peer is not None:
+                        old_peer.close()
+                cache.clear()
+                cache[key] = (self.buf, self.peer)
         self.out = torch.empty((nw, 3), dtype=torch.float32, device=dev)
 
     def smooth(self, stream=None):
@@ -231,9 +370,12 @@ class BalancedSmoother:
             self.psn.smooth_prepare(self.vol, self.mesh, self.sws, stream)
         for t in range(self.T):
             dst = self.buf[t & 1]
-            if sh.n_points:
-                self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
-            shard_halo_exchange(dst, self.windows, self.halo, self.rank, self.group)
+            if self.peer is not None:   # the step's kernel pushes the halos (every rank steps, even empty ones)
+                self.peer.step(self.vol, self.mesh, self.sws, src, dst, t & 1, self.lam, self.d, stream)
+            else:
+                if sh.n_points:
+                    self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+                shard_halo_exchange(dst, self.windows, self.halo, self.rank, self.group)
             src = dst
         if sh.n_points:
             self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, sh.halo_lo, sh.halo_lo + sh.n_points, stream)

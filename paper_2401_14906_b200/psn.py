@@ -59,6 +59,20 @@ class MeshC(ctypes.Structure):
                 ("first_point", ctypes.c_int64), ("first_quad", ctypes.c_int64), ("first_stencil", ctypes.c_int64)]
 
 
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("handle", ctypes.c_ubyte * 64), ("offset", ctypes.c_uint64)]
+
+
+class PeerSide(ctypes.Structure):
+    _fields_ = [("dst", ctypes.c_void_p * 2), ("src_begin", ctypes.c_int64), ("src_end", ctypes.c_int64),
+                ("dst_begin", ctypes.c_int64), ("peer_sig", ctypes.c_void_p)]
+
+
+class Peer(ctypes.Structure):
+    _fields_ = [("side", PeerSide * 2), ("sig", ctypes.c_void_p), ("ctr", ctypes.c_void_p), ("err", ctypes.c_void_p),
+                ("ctr_base", ctypes.c_uint64), ("iteration", ctypes.c_uint64)]
+
+
 _lib = None
 
 
@@ -112,6 +126,17 @@ def lib():
         L.psn_smooth_status.restype = ctypes.c_int
         L.psn_launch_count.argtypes = [vp]
         L.psn_launch_count.restype = i64
+        if hasattr(L, "psn_smooth_step_peer"):   # (absent from older builds loaded via PSN_LIB)
+            L.psn_smooth_step_peer.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t,
+                                               vp, vp, ctypes.c_int, ctypes.c_float, ctypes.c_float,
+                                               ctypes.POINTER(Peer), vp]
+            L.psn_smooth_step_peer.restype = ctypes.c_int
+            L.psn_ipc_export.argtypes = [vp, vp, ctypes.POINTER(IpcHandle)]
+            L.psn_ipc_export.restype = ctypes.c_int
+            L.psn_ipc_open.argtypes = [vp, ctypes.POINTER(IpcHandle), ctypes.POINTER(vp)]
+            L.psn_ipc_open.restype = ctypes.c_int
+            L.psn_ipc_close.argtypes = [vp, vp]
+            L.psn_ipc_close.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -120,7 +145,8 @@ EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_s
             "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
             "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting",
-            "psn_ctx_set_emission", "psn_ctx_set_constraint"]
+            "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_ipc_export",
+            "psn_ipc_open", "psn_ipc_close"]
 
 
 def _ptr(t):
@@ -345,6 +371,31 @@ class PSN:
         rc = self.L.psn_smooth_step(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(ws), ws.numel(), _ptr(src),
                                     _ptr(dst), float(relaxation), float(constraint), _stream(stream))
         self._check(rc)
+
+    def smooth_step_peer(self, vol: Volume, mesh: Mesh, ws: torch.Tensor, src: torch.Tensor | None,
+                         dst: torch.Tensor, parity: int, relaxation: float, constraint: float, peer: "Peer",
+                         stream=None):
+        """psn_smooth_step + the peer halo push / signal (see psn.h); `peer` is advanced in place."""
+        rc = self.L.psn_smooth_step_peer(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(ws), ws.numel(),
+                                         _ptr(src), _ptr(dst), int(parity), float(relaxation), float(constraint),
+                                         ctypes.byref(peer), _stream(stream))
+        self._check(rc)
+
+    def ipc_export(self, t: torch.Tensor) -> bytes:
+        """CUDA IPC handle (+ offset) of tensor t's memory, as bytes for the peer processes."""
+        h = IpcHandle()
+        self._check(self.L.psn_ipc_export(self.h, _ptr(t), ctypes.byref(h)))
+        return bytes(h)
+
+    def ipc_open(self, blob: bytes) -> int:
+        """Map a peer's exported memory; returns the device address (int)."""
+        h = IpcHandle.from_buffer_copy(blob)
+        p = ctypes.c_void_p()
+        self._check(self.L.psn_ipc_open(self.h, ctypes.byref(h), ctypes.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, addr: int):
+        self._check(self.L.psn_ipc_close(self.h, ctypes.c_void_p(addr)))
 
     def smooth_finalize(self, vol: Volume, mesh: Mesh, offsets: torch.Tensor | None, out: torch.Tensor,
                         w0: int = 0, w1: int | None = None, stream=None):
