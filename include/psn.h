@@ -308,6 +308,14 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
                                 size_t ws_bytes, const float *src, float *dst, int parity, float relaxation,
                                 float constraint_distance, psn_peer *peer, void *stream);
 
+/* `iterations` peer steps from the anchors in one call (no per-step host
+ * round trip): step t reads buf[(t-1)&1] (nothing at t = 0) and writes
+ * buf[t&1] with parity t&1 -- the loop every rank would otherwise run around
+ * psn_smooth_step_peer.  The result is in buf[(iterations-1)&1]. */
+psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
+                               size_t ws_bytes, float *buf0, float *buf1, int32_t iterations, float relaxation,
+                               float constraint_distance, psn_peer *peer, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -826,6 +826,23 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
     return PSN_OK;
 }
 
+psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
+                               size_t ws_bytes, float *buf0, float *buf1, int32_t iterations, float relaxation,
+                               float constraint_distance, psn_peer *peer, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    if (iterations < 0) return fail(ctx, PSN_ERR_ARG, "iterations must be >= 0");
+    int64_t launches = 0;
+    float *buf[2] = {buf0, buf1};
+    for (int32_t t = 0; t < iterations; ++t) {
+        const psn_status s = psn_smooth_step_peer(ctx, vol, mesh, ws, ws_bytes, t ? buf[(t - 1) & 1] : nullptr,
+                                                  buf[t & 1], t & 1, relaxation, constraint_distance, peer, stream);
+        if (s != PSN_OK) return s;
+        launches += ctx->launches;
+    }
+    ctx->launches = launches;
+    return PSN_OK;
+}
+
 psn_status psn_ipc_export(psn_ctx *ctx, const void *dev_ptr, psn_ipc_handle *out) {
     if (!ctx) return PSN_ERR_ARG;
     if (!dev_ptr || !out) return fail(ctx, PSN_ERR_ARG, "NULL argument");

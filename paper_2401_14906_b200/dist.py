@@ -199,6 +199,10 @@ class PeerHalo:
     def step(self, vol, mesh, ws, src, dst, parity, lam, d, stream=None):
         self.psn.smooth_step_peer(vol, mesh, ws, src, dst, parity, lam, d, self.peer, stream)
 
+    def run(self, vol, mesh, ws, iterations, lam, d, stream=None):
+        """All iterations in one library call (one launch each, no host round trip per step)."""
+        return self.psn.smooth_run_peer(vol, mesh, ws, self.bufs, iterations, lam, d, self.peer, stream)
+
     def check(self):
         if int(self.err.item()):
             raise RuntimeError("peer halo wait timed out (a neighbour stopped stepping)")
@@ -268,13 +272,12 @@ class SlabPipeline:
                     self.peer_halo.close()
                 lower, upper = peer_sides(self.rank, dist.get_world_size(self.group), slab_sends(self.table))
                 self.peer_halo, self._peer_key = PeerHalo(self.psn, self.buf, lower, upper, self.group), key
-        for t in range(self.T):
+        if self.use_peer:
+            src = self.peer_halo.run(self.vol, self.mesh, self.sws, self.T, self.lam, self.d, stream)
+        for t in range(0 if self.use_peer else self.T):
             dst = self.buf[t & 1]
-            if self.use_peer:
-                self.peer_halo.step(self.vol, self.mesh, self.sws, src, dst, t & 1, self.lam, self.d, stream)
-            else:
-                self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
-                halo_exchange(dst, self.plan, self.rank, self.group)
+            self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+            halo_exchange(dst, self.plan, self.rank, self.group)
             src = dst
         self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, 0, self.mesh.n_window, stream)
         return self.out
@@ -368,14 +371,13 @@ class BalancedSmoother:
         src = None
         if sh.n_points:
             self.psn.smooth_prepare(self.vol, self.mesh, self.sws, stream)
-        for t in range(self.T):
+        if self.peer is not None:   # the steps' kernels push the halos (every rank steps, even empty ones)
+            src = self.peer.run(self.vol, self.mesh, self.sws, self.T, self.lam, self.d, stream)
+        for t in range(0 if self.peer is not None else self.T):
             dst = self.buf[t & 1]
-            if self.peer is not None:   # the step's kernel pushes the halos (every rank steps, even empty ones)
-                self.peer.step(self.vol, self.mesh, self.sws, src, dst, t & 1, self.lam, self.d, stream)
-            else:
-                if sh.n_points:
-                    self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
-                shard_halo_exchange(dst, self.windows, self.halo, self.rank, self.group)
+            if sh.n_points:
+                self.psn.smooth_step(self.vol, self.mesh, self.sws, src, dst, self.lam, self.d, stream)
+            shard_halo_exchange(dst, self.windows, self.halo, self.rank, self.group)
             src = dst
         if sh.n_points:
             self.psn.smooth_finalize(self.vol, self.mesh, src, self.out, sh.halo_lo, sh.halo_lo + sh.n_points, stream)

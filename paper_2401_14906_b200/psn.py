@@ -131,6 +131,10 @@ def lib():
                                                vp, vp, ctypes.c_int, ctypes.c_float, ctypes.c_float,
                                                ctypes.POINTER(Peer), vp]
             L.psn_smooth_step_peer.restype = ctypes.c_int
+            L.psn_smooth_run_peer.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t,
+                                              vp, vp, ctypes.c_int32, ctypes.c_float, ctypes.c_float,
+                                              ctypes.POINTER(Peer), vp]
+            L.psn_smooth_run_peer.restype = ctypes.c_int
             L.psn_ipc_export.argtypes = [vp, vp, ctypes.POINTER(IpcHandle)]
             L.psn_ipc_export.restype = ctypes.c_int
             L.psn_ipc_open.argtypes = [vp, ctypes.POINTER(IpcHandle), ctypes.POINTER(vp)]
@@ -145,7 +149,7 @@ EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_s
             "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
             "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting",
-            "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_ipc_export",
+            "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_smooth_run_peer", "psn_ipc_export",
             "psn_ipc_open", "psn_ipc_close"]
 
 
@@ -380,6 +384,15 @@ class PSN:
                                          _ptr(src), _ptr(dst), int(parity), float(relaxation), float(constraint),
                                          ctypes.byref(peer), _stream(stream))
         self._check(rc)
+
+    def smooth_run_peer(self, vol: Volume, mesh: Mesh, ws: torch.Tensor, bufs, iterations: int, relaxation: float,
+                        constraint: float, peer: "Peer", stream=None) -> torch.Tensor:
+        """`iterations` peer steps in one call (bufs = two float4 window buffers); returns the final buffer."""
+        rc = self.L.psn_smooth_run_peer(self.h, ctypes.byref(vol), ctypes.byref(mesh.c), _ptr(ws), ws.numel(),
+                                        _ptr(bufs[0]), _ptr(bufs[1]), int(iterations), float(relaxation),
+                                        float(constraint), ctypes.byref(peer), _stream(stream))
+        self._check(rc)
+        return bufs[(iterations - 1) & 1] if iterations else None
 
     def ipc_export(self, t: torch.Tensor) -> bytes:
         """CUDA IPC handle (+ offset) of tensor t's memory, as bytes for the peer processes."""

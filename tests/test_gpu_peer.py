@@ -196,3 +196,28 @@ def test_ipc_export_open_across_processes():
     torch.cuda.synchronize()
     np.testing.assert_array_equal(view.cpu().numpy(), np.arange(1000, dtype=np.float32) * 2.0 + 1.0)
     assert float(big[:4096].abs().sum()) == 0.0 and float(big[5096:].abs().sum()) == 0.0
+
+
+def test_run_peer_single_rank_matches_single():
+    """psn_smooth_run_peer (all steps in one call) on a rank without neighbours equals
+    psn_smooth bit for bit (the multi-rank interleaving is covered step by step above:
+    in one process a rank's later steps would wait on the others)."""
+    p = gu.psn()
+    a = volume()
+    T, lam, d = 8, 0.5, 0.5
+    vols, meshes, firsts, total = extract_slabs(p, a, 1, (1.0, 1.0, 1.0))
+    ws = p.smooth_workspace(meshes[0])
+    p.smooth_prepare(vols[0], meshes[0], ws)
+    bufs = [p.offsets_buffer(meshes[0].n_window, "cuda") for _ in range(2)]
+    sig = torch.zeros(2, dtype=torch.int64, device="cuda")
+    ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pr = Peer()
+    pr.sig, pr.ctr, pr.err = sig.data_ptr(), ctr.data_ptr(), err.data_ptr()
+    res = p.smooth_run_peer(vols[0], meshes[0], ws, bufs, T, lam, d, pr)
+    out = torch.empty((meshes[0].n_window, 3), dtype=torch.float32, device="cuda")
+    p.smooth_finalize(vols[0], meshes[0], res, out)
+    _, vol1, m1, _ = gu.gpu_extract(a)
+    s1 = p.smooth(vol1, m1, T, lam, d)
+    np.testing.assert_array_equal(out[:m1.n_points].cpu().numpy(), s1[:m1.n_points].cpu().numpy())
+    assert pr.iteration == T and int(err.item()) == 0
