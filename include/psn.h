@@ -163,8 +163,8 @@ psn_status psn_smooth_workspace(const psn_mesh *mesh, size_t *bytes);
 /* Build the smoothing cache of `mesh` into ws (psn_smooth does this itself;
  * slab users call it once before their psn_smooth_step loop).  `vol` (dims)
  * selects the cache form: the packed 8-byte one (id distances to the y/z
- * neighbours) when M-1 < 2^10 and (M-1)(N-1) < 2^21 under the box
- * constraint, else 16 bytes per point.  psn_smooth_step must be given the
+ * neighbours) when M-1 < 2^10 and (M-1)(N-1) < 2^21, else 16 bytes per
+ * point.  psn_smooth_step must be given the
  * same volume.  PSN_ERR_ARG: NULL volume / mesh arrays, workspace too small. */
 psn_status psn_smooth_prepare(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, void *ws, size_t ws_bytes,
                               void *stream);
@@ -192,9 +192,9 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
  * entries of dst (same layout; w written as 0).  ws must hold the smoothing
  * cache built by psn_smooth_prepare for the same `vol`.  src == NULL means
  * "all offsets zero" (first iteration from the anchors).  Same kernel and
- * bits as psn_smooth's per-iteration path.  Box constraint only
- * (PSN_ERR_ARG in sphere mode); PSN_ERR_ARG for NULL dst / vol, misaligned
- * buffers or a workspace too small.
+ * bits as psn_smooth's per-iteration path (box or sphere constraint, as set
+ * on the context).  PSN_ERR_ARG for NULL dst / vol, misaligned buffers or a
+ * workspace too small.
  */
 psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws, size_t ws_bytes,
                            const float *src, float *dst, float relaxation, float constraint_distance, void *stream);
@@ -219,12 +219,11 @@ enum { PSN_COUNT_AUTO = 0, PSN_COUNT_XTILE = 1 };
 psn_status psn_ctx_set_counting(psn_ctx *ctx, int mode);
 
 /* Constraint on the total motion of a point relative to its voxel centre
- * used by psn_smooth:
+ * used by psn_smooth, psn_smooth_step and psn_smooth_step_peer:
  *   PSN_CONSTRAINT_BOX (default): |p - anchor|_a <= d * s_a per axis (reading Q10);
  *   PSN_CONSTRAINT_SPHERE: |p - anchor| <= d * min(s), radial projection after
  *     the lambda step ("a constraint sphere centered at the voxel center
- *     point", reading Q26).  psn_smooth_step (slab path) supports the box only
- *     and returns PSN_ERR_ARG in sphere mode. */
+ *     point", reading Q26). */
 enum { PSN_CONSTRAINT_BOX = 0, PSN_CONSTRAINT_SPHERE = 1 };
 psn_status psn_ctx_set_constraint(psn_ctx *ctx, int shape);
 

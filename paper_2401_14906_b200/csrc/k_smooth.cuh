@@ -187,6 +187,7 @@ struct SmoothV4 {
     uint32_t n_own, halo_lo;
     float lambda, d;
     double sp[3], org[3];
+    Constraint cons;           // used by k_smooth_v4<..., SPHERE = true> only (reading Q26)
     PeerArgs peer;             // used by k_smooth_v4<..., PEER = true> only
 };
 
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, cons
     }
 }
 
-template <bool PACKED, bool PREF = false, bool PEER = false>
+template <bool PACKED, bool PREF = false, bool PEER = false, bool SPHERE = false>
 __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
@@ -288,8 +289,13 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
             if ((f & 4u) && lane == 0) { const float4 v = __ldg(src + w - 1u); mx = make_float3(v.x, v.y, v.z); }
             if ((f & 8u) && (lane == 31 || i + 1u >= n)) { const float4 v = __ldg(src + w + 1u); px = make_float3(v.x, v.y, v.z); }
         }
-        const float3 r = jacobi_update_box(f, o, mx, px, make_float3(h0.x, h0.y, h0.z), make_float3(h1.x, h1.y, h1.z),
-                                           make_float3(h2.x, h2.y, h2.z), make_float3(h3.x, h3.y, h3.z), a.lambda, a.d);
+        float3 r;
+        if constexpr (SPHERE)   // sphere of radius d*min(s) about the anchor (reading Q26)
+            r = jacobi_update_t<true>(f, o, mx, px, make_float3(h0.x, h0.y, h0.z), make_float3(h1.x, h1.y, h1.z),
+                                      make_float3(h2.x, h2.y, h2.z), make_float3(h3.x, h3.y, h3.z), a.lambda, a.cons);
+        else
+            r = jacobi_update_box(f, o, mx, px, make_float3(h0.x, h0.y, h0.z), make_float3(h1.x, h1.y, h1.z),
+                                  make_float3(h2.x, h2.y, h2.z), make_float3(h3.x, h3.y, h3.z), a.lambda, a.d);
         if (a.world) {
             a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
             a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
@@ -316,68 +322,6 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
                 for (int s = 0; s < 2; ++s)
                     if (a.peer.side[s].dst) st_release_sys64(a.peer.side[s].peer_sig, a.peer.g + 1);
             }
-        }
-    }
-}
-
-// Same step with the sphere constraint (separate kernel: the box kernel stays minimal).
-struct SmoothSoASphere {   // k_smooth_soa_sphere: SoA offsets, sphere constraint (reading Q26)
-    const float *src;          // SoA window offsets; NULL = all zero (first iteration)
-    float *dst;                // SoA window offsets (own entries written)
-    float *world;              // if non-NULL: write AoS world coordinates here instead of dst
-    const uint8_t *fmask;
-    const uint4 *nbr;
-    const float *points;
-    uint32_t n_own, halo_lo, ws;
-    float lambda;
-    Constraint cons;
-    double sp[3], org[3];
-};
-
-__global__ void __launch_bounds__(256) k_smooth_soa_sphere(SmoothSoASphere a) {
-    constexpr bool SPHERE = true;
-    const int lane = threadIdx.x & 31;
-    const uint32_t n = a.n_own, ws = a.ws;
-    const float *__restrict__ sx = a.src, *__restrict__ sy = a.src + ws, *__restrict__ sz = a.src + 2 * ws;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    Constraint cons;   // register copy (box: only d is live)
-    cons.d = a.cons.d;
-    cons.sphere = SPHERE;
-    if (SPHERE) { cons.r = a.cons.r; cons.r2 = a.cons.r2; cons.sx = a.cons.sx; cons.sy = a.cons.sy; cons.sz = a.cons.sz; }
-    else { cons.r = cons.r2 = cons.sx = cons.sy = cons.sz = 0.f; }
-    const float lambda = a.lambda;
-    // uniform trip count so that every lane takes part in the shuffles
-    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
-        const uint32_t i = base + lane;
-        const bool act = i < n;
-        const uint32_t ii = act ? i : n - 1u;
-        const uint32_t w = a.halo_lo + ii;
-        const uint4 nbw = __ldg(a.nbr + ii);
-        const uint32_t f = act ? nbr_faces(nbw) : 0u;
-        const uint4 nb = nbr_idx(nbw);
-        float3 o = make_float3(0.f, 0.f, 0.f), g0 = o, g1 = o, g2 = o, g3 = o;
-        if (a.src) {
-            o = make_float3(__ldg(sx + w), __ldg(sy + w), __ldg(sz + w));
-            g0 = make_float3(__ldg(sx + nb.x), __ldg(sy + nb.x), __ldg(sz + nb.x));
-            g1 = make_float3(__ldg(sx + nb.y), __ldg(sy + nb.y), __ldg(sz + nb.y));
-            g2 = make_float3(__ldg(sx + nb.z), __ldg(sy + nb.z), __ldg(sz + nb.z));
-            g3 = make_float3(__ldg(sx + nb.w), __ldg(sy + nb.w), __ldg(sz + nb.w));
-        }
-        float3 mx, px;
-        mx.x = __shfl_up_sync(kFull, o.x, 1); mx.y = __shfl_up_sync(kFull, o.y, 1); mx.z = __shfl_up_sync(kFull, o.z, 1);
-        px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
-        if (!act) continue;
-        if (a.src && f) {
-            if ((f & 4u) && lane == 0) mx = make_float3(__ldg(sx + w - 1u), __ldg(sy + w - 1u), __ldg(sz + w - 1u));
-            if ((f & 8u) && (lane == 31 || i + 1u >= n)) px = make_float3(__ldg(sx + w + 1u), __ldg(sy + w + 1u), __ldg(sz + w + 1u));
-        }
-        const float3 r = jacobi_update_t<true>(f, o, mx, px, g0, g1, g2, g3, lambda, cons);
-        if (a.world) {
-            a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
-            a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
-            a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
-        } else {
-            a.dst[w] = r.x; a.dst[ws + w] = r.y; a.dst[2 * ws + w] = r.z;
         }
     }
 }

@@ -177,6 +177,11 @@ cudaError_t launch_count(const CountArgs &ca, int64_t blocks, int threads, size_
     return cudaGetLastError();
 }
 
+using V4Fn = void (*)(SmoothV4);
+template <bool PK, bool PF, bool PE> V4Fn v4_sel(bool sphere) {
+    return sphere ? k_smooth_v4<PK, PF, PE, true> : k_smooth_v4<PK, PF, PE, false>;
+}
+
 template <typename T, bool ANZ, int CPL, int RPW>
 cudaError_t launch_count3(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
     static size_t attr_set = 0;
@@ -493,7 +498,6 @@ psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, 
 }
 
 namespace {
-int64_t soa_stride(int64_t nw) { return (std::max<int64_t>(nw, 1) + 31) / 32 * 32; }
 struct SmoothLayout { size_t nbr, buf0, buf1, rng, done, sch, total; int64_t nw, U; };
 // [nbr uint4 x P | buf0 float4 x W | buf1 float4 x W | rng int2 x U | done u32 x U | sched]
 SmoothLayout smooth_layout(const psn_mesh *m) {
@@ -502,8 +506,8 @@ SmoothLayout smooth_layout(const psn_mesh *m) {
     L.U = (m->n_points + kTbTileMin - 1) / kTbTileMin;   // schedule arrays sized for the smallest tile
     L.nbr = 0;
     L.buf0 = align_up(16 * (size_t)std::max<int64_t>(m->n_points, 1));
-    // offset buffers: float4 [W] (wavefront) or SoA float [3][ws] (per-iteration), ws = W rounded to 32
-    const size_t bufb = std::max<size_t>(16 * (size_t)std::max<int64_t>(L.nw, 1), 12 * (size_t)soa_stride(L.nw));
+    // offset buffers: float4 [W]
+    const size_t bufb = 16 * (size_t)std::max<int64_t>(L.nw, 1);
     L.buf1 = L.buf0 + align_up(bufb);
     L.rng = L.buf1 + align_up(bufb);
     L.done = L.rng + align_up(8 * (size_t)std::max<int64_t>(L.U, 1));
@@ -549,10 +553,10 @@ int64_t grid_for(psn_ctx *ctx, int64_t n) {
     return std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 16));
 }
 
-// Packed 8-byte smoothing cache (k_smooth_prep8) for the box constraint when the volume's
-// rows / layers keep neighbour id distances within its fields: y < 2^10, z < 2^21.
-bool smooth_packed(const psn_ctx *ctx, const psn_volume *vol) {
-    if (!vol || ctx->constraint != PSN_CONSTRAINT_BOX || getenv("PSN_SMOOTH_NBR16")) return false;
+// Packed 8-byte smoothing cache (k_smooth_prep8) when the volume's rows / layers keep
+// neighbour id distances within its fields: y < 2^10, z < 2^21.
+bool smooth_packed(const psn_ctx *, const psn_volume *vol) {
+    if (!vol || getenv("PSN_SMOOTH_NBR16")) return false;
     const int64_t Mc = vol->dims[0] - 1, Nc = vol->dims[1] - 1;
     return Mc < (1 << 10) && Mc * Nc < (1 << 21);
 }
@@ -567,14 +571,28 @@ psn_status launch_prep8(psn_ctx *ctx, const psn_mesh *mesh, void *ws, cudaStream
     return cuda_check(ctx, "smooth prep launch");
 }
 
-SmoothV4 smooth_v4_args(const psn_volume *vol, const psn_mesh *mesh, const void *ws, float lambda, float d) {
+SmoothV4 smooth_v4_args(const psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws, float lambda,
+                        float d) {
     SmoothV4 v;
     memset(&v, 0, sizeof(v));
     v.nbr = static_cast<const uint4 *>(ws); v.nbr8 = static_cast<const uint2 *>(ws); v.points = mesh->points;
     v.n_own = (uint32_t)mesh->n_points; v.halo_lo = (uint32_t)mesh->halo_lo_points;
     v.lambda = lambda; v.d = d;
+    v.cons = make_constraint(ctx->constraint, d, vol->spacing);
     for (int c = 0; c < 3; ++c) { v.sp[c] = vol->spacing[c]; v.org[c] = vol->origin[c]; }
     return v;
+}
+
+// The k_smooth_v4 instantiation for (cache form, one-step-ahead cache loads, peer push, sphere).
+V4Fn pick_v4(bool packed, bool pref, bool peer, bool sphere) {
+    if (peer) return packed ? v4_sel<true, false, true>(sphere) : v4_sel<false, false, true>(sphere);
+    if (packed) return pref ? v4_sel<true, true, false>(sphere) : v4_sel<true, false, false>(sphere);
+    return v4_sel<false, false, false>(sphere);
+}
+int64_t v4_grid(psn_ctx *ctx, V4Fn kern, int64_t n) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+    return std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
 }
 
 psn_status launch_prep(psn_ctx *ctx, const psn_mesh *mesh, void *ws, cudaStream_t st) {
@@ -631,47 +649,20 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     if ((s = packed ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
         // one launch per Jacobi iteration, offsets double-buffered in the two buffer slots
-        if (!cons.sphere) {   // box constraint: float4 offsets (one 16-byte load per gather)
-            SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
-            float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
-            // one-step-ahead cache loads: measured faster up to tens of millions of points (c6
-            // -8 %, c4 -3 %) and slower on c5a's 133 M (+8 %), where the step is closest to
-            // the DRAM bound; chosen by size
-            void (*kern)(SmoothV4) = packed ? (nw < (1ll << 26) ? k_smooth_v4<true, true> : k_smooth_v4<true, false>)
-                                            : k_smooth_v4<false, false>;
-            int occ4 = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, kern, 256, 0);
-            const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ4, 1)));
-            const float4 *s4 = nullptr;
-            for (int32_t t = 0; t < iterations; ++t) {
-                const bool last = (t == iterations - 1);
-                v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
-                kern<<<(unsigned)g4, 256, 0, st>>>(v);
-                ++ctx->launches;
-                s4 = v.dst;
-            }
-            return cuda_check(ctx, "smooth launch");
-        }
-        // sphere constraint: SoA offsets (k_smooth_soa_sphere)
-        SmoothSoASphere b;
-        memset(&b, 0, sizeof(b));
-        b.fmask = mesh->face_masks; b.nbr = static_cast<const uint4 *>(ws); b.points = mesh->points;
-        b.n_own = (uint32_t)mesh->n_points; b.halo_lo = (uint32_t)mesh->halo_lo_points;
-        b.ws = (uint32_t)soa_stride(SL.nw);
-        b.lambda = relaxation; b.cons = cons;
-        for (int c = 0; c < 3; ++c) { b.sp[c] = vol->spacing[c]; b.org[c] = vol->origin[c]; }
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_smooth_soa_sphere, 256, 0);
-        const int64_t gsoa = std::max<int64_t>(1, std::min<int64_t>((nw + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
-        float *buf[2] = {at<float>(ws, SL.buf0), at<float>(ws, SL.buf1)};
-        const float *src = nullptr;
+        SmoothV4 v = smooth_v4_args(ctx, vol, mesh, ws, relaxation, constraint_distance);
+        float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
+        // one-step-ahead cache loads: measured faster up to tens of millions of points (c6
+        // -8 %, c4 -3 %) and slower on c5a's 133 M (+8 %), where the step is closest to the
+        // DRAM bound; chosen by size
+        const V4Fn kern = pick_v4(packed, packed && nw < (1ll << 26), false, cons.sphere != 0);
+        const int64_t g4 = v4_grid(ctx, kern, nw);
+        const float4 *s4 = nullptr;
         for (int32_t t = 0; t < iterations; ++t) {
             const bool last = (t == iterations - 1);
-            float *dst = last ? nullptr : buf[t & 1];
-            b.src = src; b.dst = dst; b.world = last ? out : nullptr;
-            k_smooth_soa_sphere<<<(unsigned)gsoa, 256, 0, st>>>(b);
+            v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
+            kern<<<(unsigned)g4, 256, 0, st>>>(v);
             ++ctx->launches;
-            src = dst;
+            s4 = v.dst;
         }
         return cuda_check(ctx, "smooth launch");
     }
@@ -760,22 +751,17 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *
     psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
     if (s != PSN_OK) return s;
     if (!dst || !vol) return fail(ctx, PSN_ERR_ARG, "dst / volume is NULL");
-    if (ctx->constraint != PSN_CONSTRAINT_BOX)
-        return fail(ctx, PSN_ERR_ARG, "psn_smooth_step supports the box constraint (the sphere needs psn_smooth)");
     if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
     if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u)
         return fail(ctx, PSN_ERR_ARG, "offset buffers must be 16-byte aligned (float4 entries)");
     if (mesh->n_points == 0) return PSN_OK;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
-    SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
+    SmoothV4 v = smooth_v4_args(ctx, vol, mesh, ws, relaxation, constraint_distance);
     v.src = reinterpret_cast<const float4 *>(src); v.dst = reinterpret_cast<float4 *>(dst); v.world = nullptr;
     const bool packed = smooth_packed(ctx, vol);   // the form psn_smooth_prepare built for this volume
-    void (*kern)(SmoothV4) = packed ? (mesh->n_points < (1ll << 26) ? k_smooth_v4<true, true> : k_smooth_v4<true, false>)
-                                    : k_smooth_v4<false, false>;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
-    const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
-    kern<<<(unsigned)g4, 256, 0, static_cast<cudaStream_t>(stream)>>>(v);
+    const V4Fn kern = pick_v4(packed, packed && mesh->n_points < (1ll << 26), false,
+                              ctx->constraint == PSN_CONSTRAINT_SPHERE);
+    kern<<<(unsigned)v4_grid(ctx, kern, mesh->n_points), 256, 0, static_cast<cudaStream_t>(stream)>>>(v);
     ++ctx->launches;
     return cuda_check(ctx, "smooth step launch");
 }
@@ -790,13 +776,11 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
     if (!dst || !vol || !peer || !peer->sig || !peer->ctr || !peer->err)
         return fail(ctx, PSN_ERR_ARG, "dst / volume / peer descriptor is NULL");
     if (parity != 0 && parity != 1) return fail(ctx, PSN_ERR_ARG, "parity must be 0 or 1");
-    if (ctx->constraint != PSN_CONSTRAINT_BOX)
-        return fail(ctx, PSN_ERR_ARG, "psn_smooth_step_peer supports the box constraint");
     if (!ws || ws_bytes < smooth_layout(mesh).buf0) return fail(ctx, PSN_ERR_ARG, "smoothing workspace too small");
     if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u)
         return fail(ctx, PSN_ERR_ARG, "offset buffers must be 16-byte aligned (float4 entries)");
     const int64_t own0 = mesh->halo_lo_points, own1 = own0 + mesh->n_points;
-    SmoothV4 v = smooth_v4_args(vol, mesh, ws, relaxation, constraint_distance);
+    SmoothV4 v = smooth_v4_args(ctx, vol, mesh, ws, relaxation, constraint_distance);
     v.src = reinterpret_cast<const float4 *>(src); v.dst = reinterpret_cast<float4 *>(dst); v.world = nullptr;
     for (int k = 0; k < 2; ++k) {
         const psn_peer_side &ps = peer->side[k];
@@ -810,11 +794,8 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
         o.peer_sig = ps.peer_sig;
     }
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
-    const bool packed = smooth_packed(ctx, vol);
-    void (*kern)(SmoothV4) = packed ? k_smooth_v4<true, false, true> : k_smooth_v4<false, false, true>;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
-    const int64_t g4 = std::max<int64_t>(1, std::min<int64_t>((mesh->n_points + 255) / 256, (int64_t)ctx->sms * std::max(occ, 1)));
+    const V4Fn kern = pick_v4(smooth_packed(ctx, vol), false, true, ctx->constraint == PSN_CONSTRAINT_SPHERE);
+    const int64_t g4 = v4_grid(ctx, kern, mesh->n_points);
     v.peer.sig = peer->sig; v.peer.ctr = reinterpret_cast<unsigned long long *>(peer->ctr); v.peer.err = peer->err;
     v.peer.ctr_last = (unsigned long long)(peer->ctr_base + (uint64_t)g4 - 1);
     v.peer.g = peer->iteration;

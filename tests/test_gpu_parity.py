@@ -215,17 +215,6 @@ def test_degenerate_and_errors():
     with pytest.raises(PSNError) as e:
         p.triangulate(mesh, mesh.points, strategy=4)
     assert e.value.status == PSN_ERR_ARG
-    # the slab smoothing step supports the box constraint only
-    try:
-        p.set_constraint(1)
-        ws = p.smooth_workspace(mesh)
-        p.smooth_prepare(vol, mesh, ws)
-        dst = p.offsets_buffer(mesh.n_window, "cuda")
-        with pytest.raises(PSNError) as e:
-            p.smooth_step(vol, mesh, ws, None, dst, 0.5, 0.5)
-        assert e.value.status == PSN_ERR_ARG
-    finally:
-        p.set_constraint(0)
     # float4 offset buffers must be 16-byte aligned
     ws = p.smooth_workspace(mesh)
     p.smooth_prepare(vol, mesh, ws)
@@ -285,6 +274,33 @@ def test_wavefront_smoothing_bit_identical(G, tile):
             assert err.max() <= TOL
     finally:
         p.set_smoothing(1, 0, 0)
+
+
+@pytest.mark.parametrize("shape", [0, 1])
+def test_step_loop_matches_psn_smooth(shape):
+    """psn_smooth_prepare + T x psn_smooth_step (+ finalize), the slab path on a whole
+    volume, gives psn_smooth's bits for the box and the sphere constraint."""
+    p = gu.psn()
+    rng = np.random.default_rng(55)
+    a = rng.integers(0, 3, size=(14, 17, 23)).astype(np.uint8)
+    _, vol, mesh, _ = gu.gpu_extract(a, spacing=(0.8, 1.0, 1.5))
+    try:
+        p.set_constraint(shape)
+        T = 8
+        ws = p.smooth_workspace(mesh)
+        ref = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()
+        p.smooth_prepare(vol, mesh, ws)
+        bufs = [p.offsets_buffer(mesh.n_window, "cuda") for _ in range(2)]
+        src = None
+        for t in range(T):
+            p.smooth_step(vol, mesh, ws, src, bufs[t & 1], 0.5, 0.5)
+            src = bufs[t & 1]
+        out = torch.empty_like(ref)
+        p.smooth_finalize(vol, mesh, src, out)
+        n = mesh.n_points
+        assert torch.equal(out[:n], ref[:n])
+    finally:
+        p.set_constraint(0)
 
 
 def test_packed_smoothing_cache_bit_identical(monkeypatch):
