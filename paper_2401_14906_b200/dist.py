@@ -179,22 +179,35 @@ class PeerHalo:
         self.ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         torch.cuda.synchronize(dev)   # zeroed before any neighbour can signal
-        mine = [psn.ipc_export(bufs[0]), psn.ipc_export(bufs[1]), psn.ipc_export(self.sig)]
+        try:
+            mine = [psn.ipc_export(bufs[0]), psn.ipc_export(bufs[1]), psn.ipc_export(self.sig)]
+        except Exception:   # e.g. memory not from cudaMalloc: every rank must then fall back together
+            mine = None
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
+        if any(h is None for h in allh):
+            raise ValueError("CUDA IPC export failed on some rank")
         self.peer = Peer()
         self.peer.sig, self.peer.ctr, self.peer.err = self.sig.data_ptr(), self.ctr.data_ptr(), self.err.data_ptr()
         self.opened = []
-        for k, (nb, spec) in enumerate(((rank - 1, lower), (rank + 1, upper))):
-            if spec is None:
-                continue
-            b0, b1, sg = (psn.ipc_open(h) for h in allh[nb])
-            self.opened += [b0, b1, sg]
-            side = self.peer.side[k]
-            side.dst[0], side.dst[1] = b0, b1
-            side.src_begin, side.src_end, side.dst_begin = spec
-            side.peer_sig = sg + 8 * (1 - k)   # pushes down land in the lower rank's sig[1], up in sig[0]
-        dist.barrier(group=group)   # every rank mapped its neighbours before anyone signals
+        ok = True
+        try:
+            for k, (nb, spec) in enumerate(((rank - 1, lower), (rank + 1, upper))):
+                if spec is None:
+                    continue
+                b0, b1, sg = (psn.ipc_open(h) for h in allh[nb])
+                self.opened += [b0, b1, sg]
+                side = self.peer.side[k]
+                side.dst[0], side.dst[1] = b0, b1
+                side.src_begin, side.src_end, side.dst_begin = spec
+                side.peer_sig = sg + 8 * (1 - k)   # pushes down land in the lower rank's sig[1], up in sig[0]
+        except Exception:
+            ok = False
+        oks = [None] * world
+        dist.all_gather_object(oks, ok, group=group)   # also: every rank mapped its neighbours before anyone signals
+        if not all(oks):
+            self.close()
+            raise ValueError("CUDA IPC open failed on some rank")
 
     def step(self, vol, mesh, ws, src, dst, parity, lam, d, stream=None):
         self.psn.smooth_step_peer(vol, mesh, ws, src, dst, parity, lam, d, self.peer, stream)
@@ -270,9 +283,12 @@ class SlabPipeline:
             if self.peer_halo is None or self._peer_key != key:
                 if self.peer_halo is not None:
                     self.peer_halo.close()
-                lower, upper = peer_sides(self.rank, dist.get_world_size(self.group), slab_sends(self.table))
-                self.peer_halo, self._peer_key = PeerHalo(self.psn, self.buf, lower, upper, self.group), key
-        if self.use_peer:
+                try:
+                    lower, upper = peer_sides(self.rank, dist.get_world_size(self.group), slab_sends(self.table))
+                    self.peer_halo, self._peer_key = PeerHalo(self.psn, self.buf, lower, upper, self.group), key
+                except ValueError:   # consistent on every rank: C2 over NCCL from now on
+                    self.use_peer, self.peer_halo = False, None
+        if self.use_peer and self.peer_halo is not None:
             src = self.peer_halo.run(self.vol, self.mesh, self.sws, self.T, self.lam, self.d, stream)
         for t in range(0 if self.use_peer else self.T):
             dst = self.buf[t & 1]
