@@ -116,6 +116,13 @@ typedef struct {
     int64_t n_points, n_quads, n_stencil;        /* out: this call's own totals */
     int64_t halo_lo_points, halo_hi_points;      /* out: points in layers own_k0-1 / own_k1 */
     int64_t first_point, first_quad, first_stencil;  /* in (EMIT) */
+    /* optional: uint32[cap_points][2] packed smoothing cache of the own points (see
+     * psn_smooth_prepare).  When non-NULL, PSN_EMIT writes it alongside the
+     * stencils if the volume allows the packed form and the band-staged
+     * emission runs, and sets smooth_cache_valid = 1 (else 0); psn_smooth then
+     * skips building the cache (saves reading the CSR back). */
+    uint32_t *smooth_cache;
+    int64_t smooth_cache_valid;                  /* out (EMIT) */
 } psn_mesh;
 
 psn_status psn_ctx_create(int device, psn_ctx **out);

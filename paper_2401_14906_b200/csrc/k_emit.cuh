@@ -15,6 +15,7 @@
 // the disjoint preallocated slots given by the scan -- no atomics.
 #pragma once
 #include "k_scan.cuh"
+#include "k_smooth.cuh"
 #include "psn_common.cuh"
 
 namespace psn {
@@ -33,6 +34,7 @@ struct EmitArgs {
     int64_t cap_points, cap_quads, cap_stencil;
     uint32_t first_point, first_quad, first_stencil;
     ScanHeader *hdr;
+    uint2 *scache;             // if non-NULL (k_emit_band): packed smoothing cache of the own points
 };
 
 __device__ __forceinline__ float anchor_coord(double org, double sp, int64_t idx) {
@@ -971,6 +973,9 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
                 const uint32_t s0 = sbase0 + run_s + (ex & 0xffffu);
                 a.fmask[o] = (uint8_t)fm;
                 a.csr_off[o] = a.first_stencil + s0;
+                if (a.scache)   // the smoothing cache k_smooth_prep8 would build from these stencil entries
+                    a.scache[o] = nbr8_pack(g, make_uint4((fm & 1u) ? gn[1] : g, (fm & 2u) ? gn[2] : g,
+                                                          (fm & 16u) ? gn[3] : g, (fm & 32u) ? gn[4] : g), fm);
                 uint32_t *sc = stage ? scsr[warp] + (ex & 0xffffu) : a.csr_ids + s0;
                 if (fm & 1u) *sc++ = gn[1];      // -z  (j, k-1)
                 if (fm & 2u) *sc++ = gn[2];      // -y  (j-1, k)

@@ -309,6 +309,10 @@ psn_status psn_extract_workspace(const psn_volume *vol, size_t *bytes) {
     return PSN_OK;
 }
 
+namespace {
+bool smooth_packed(const psn_ctx *, const psn_volume *vol);   // below, with the smoothing entry points
+}
+
 psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *labels, psn_mesh *mesh,
                        unsigned phase, void *ws, size_t ws_bytes, void *stream) {
     if (!ctx) return PSN_ERR_ARG;
@@ -449,9 +453,15 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.first_point = (uint32_t)mesh->first_point; ea.first_quad = (uint32_t)mesh->first_quad;
     ea.first_stencil = (uint32_t)mesh->first_stencil;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
+    ea.scache = nullptr;
+    mesh->smooth_cache_valid = 0;
     int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * 16));
     const int emode = ctx->emit_mode;
     if (L.W32 <= 32 && emode == 0) {   // k_emit_band: one resident wave of CTAs looping over bands
+        if (mesh->smooth_cache && smooth_packed(ctx, vol)) {   // the packed smoothing cache rides along
+            ea.scache = reinterpret_cast<uint2 *>(mesh->smooth_cache);
+            mesh->smooth_cache_valid = 1;
+        }
         int occ = 0;
         const void *fn = eb == 1 ? (anz ? (const void *)k_emit_band<uint8_t, true> : (const void *)k_emit_band<uint8_t, false>)
                        : eb == 2 ? (anz ? (const void *)k_emit_band<uint16_t, true> : (const void *)k_emit_band<uint16_t, false>)
@@ -646,10 +656,13 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     }
     const Constraint cons = make_constraint(ctx->constraint, constraint_distance, vol->spacing);
     const bool packed = ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION && smooth_packed(ctx, vol);
-    if ((s = packed ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
+    // the packed cache written by the emission, if any, replaces the prep pass
+    const bool cached = packed && mesh->smooth_cache && mesh->smooth_cache_valid;
+    if (!cached && (s = packed ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
         // one launch per Jacobi iteration, offsets double-buffered in the two buffer slots
         SmoothV4 v = smooth_v4_args(ctx, vol, mesh, ws, relaxation, constraint_distance);
+        if (cached) v.nbr8 = reinterpret_cast<const uint2 *>(mesh->smooth_cache);
         float4 *b4[2] = {at<float4>(ws, SL.buf0), at<float4>(ws, SL.buf1)};
         // one-step-ahead cache loads: measured faster up to tens of millions of points (c6
         // -8 %, c4 -3 %) and slower on c5a's 133 M (+8 %), where the step is closest to the

@@ -313,14 +313,29 @@ def test_packed_smoothing_cache_bit_identical(monkeypatch):
             rng.integers(0, 3, size=(4, 9, 1024)).astype(np.uint16),
             psn_gen.generate_host(psn_gen.config("c2"))[100:140]]
     for a in vols:
-        _, vol, mesh, _ = gu.gpu_extract(a, spacing=(0.8, 1.0, 1.5))
+        dev = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        vol = p.volume(dev, spacing=(0.8, 1.0, 1.5))
+        labels, ws_e = p.labels(None), p.workspace(vol)
+        counted = p.count(vol, labels, ws_e)
+        mesh = p.alloc_mesh(counted.n_points, counted.n_points, counted.n_quads, counted.n_stencil, smooth_cache=True)
+        mesh = p.emit(vol, labels, ws_e, counted, mesh=mesh)
+        assert mesh.c.smooth_cache_valid == 1          # written by the emission (band kernel, packable dims)
         ws = p.smooth_workspace(mesh)
-        packed = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws).clone()
+        packed = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws).clone()   # uses the emission's cache
+        mesh.c.smooth_cache_valid = 0
+        prep = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws).clone()     # k_smooth_prep8 builds it from the CSR
+        mesh.c.smooth_cache_valid = 1
         monkeypatch.setenv("PSN_SMOOTH_NBR16", "1")
         wide = p.smooth(vol, mesh, 9, 0.5, 0.5, ws=ws)
         monkeypatch.delenv("PSN_SMOOTH_NBR16")
         n = mesh.n_points
+        assert torch.equal(packed[:n], prep[:n])
         assert torch.equal(packed[:n], wide[:n])
+        # the emitted cache equals the one the prep kernel builds (same bits)
+        ws2 = p.smooth_workspace(mesh)
+        p.smooth_prepare(vol, mesh, ws2)
+        built = ws2[:8 * n].view(torch.int32).view(n, 2)
+        assert torch.equal(built, mesh.smooth_cache[:n])
 
 
 def test_dense_wide_rows_and_layers_smoothing():
