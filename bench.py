@@ -281,6 +281,8 @@ def run_psn(args, rank, world, local_rank):
 
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    L2_BYTES = 126e6
+    flush = torch.empty(int(2 * L2_BYTES), dtype=torch.uint8, device=dev) if V * b <= L2_BYTES else None
     barrier()
     torch.cuda.synchronize()
     clk.__enter__()
@@ -289,6 +291,8 @@ def run_psn(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clk.mark(True)
     for s in range(K):
+        if flush is not None:   # inputs fit in L2: flush it between timed steps (outside the events)
+            flush.zero_()
         ev[s][0].record(stream)
         run_extract()
         ev[s][1].record(stream)
@@ -371,7 +375,7 @@ def run_psn(args, rank, world, local_rank):
             cpu = {"value": None, "unit": "voxel/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
     if rank == 0:
-        l2 = 126e6
+        l2 = L2_BYTES
         line = {
             "metric": METRIC, "value": value, "unit": "voxel/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -383,7 +387,7 @@ def run_psn(args, rank, world, local_rank):
                                           else ", halo: NCCL point-to-point"))
                        if world > 1 else "single GPU",
                        "l2": ("inputs larger than L2 (%.2f GB labels, %.2f GB smoothing state)" % (V * b / 1e9, P * 28 / 1e9))
-                       if V * b > l2 else "inputs fit in L2 (no flush; absolute numbers only)"},
+                       if V * b > l2 else "inputs fit in L2: L2 flushed (2x L2 written) before every timed step"},
             "counts": {"points": P, "quads": Q, "stencil": S},
             "extract": {"ms": t_ext, "voxels_per_s": ext_vps, "bytes_alg": b_ext, "gbs": ext_gbs, "frac": ext_gbs / world / peak},
             "smooth": {"ms": t_sm, "pt_iters_per_s": sm_ptit, "bytes_alg_per_iter": b_sm, "gbs": sm_gbs,
