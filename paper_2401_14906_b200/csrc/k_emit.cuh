@@ -795,14 +795,15 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
         };
         const BandBuf &bb = buf[sb];
         const int32_t rr0 = band * B;
-        // staged-row accessors (element shifts of each range's aligned copy)
-        const int32_t sh_m[3] = {elem_shift(rr0 + rstart[0], 0, 4, W32), elem_shift(rr0 + rstart[1], 0, 4, W32),
-                                 elem_shift(rr0 + rstart[2], 0, 4, W32)};
-        const int32_t sh_p[3] = {elem_shift(rr0 + rstart[0], 0, 2, W32), elem_shift(rr0 + rstart[1], 0, 2, W32),
-                                 elem_shift(rr0 + rstart[2], 0, 2, W32)};
-        const int32_t sh_o[3] = {elem_shift(rr0 + rstart[0], 0, 4, 1), elem_shift(rr0 + rstart[1], 0, 4, 1),
-                                 elem_shift(rr0 + rstart[2], 0, 4, 1)};
-        const int32_t sh_r = elem_shift(rr0, 0, 4, 1);
+        // staged-row accessors: element shifts of each range's 16-byte-aligned copy (the low bits
+        // of the first element's index -- 32-bit wrap-around keeps them exact)
+        const uint32_t e_m[3] = {(uint32_t)(rr0 + rstart[0]) * (uint32_t)W32, (uint32_t)(rr0 + rstart[1]) * (uint32_t)W32,
+                                 (uint32_t)(rr0 + rstart[2]) * (uint32_t)W32};
+        const int32_t sh_m[3] = {(int32_t)(e_m[0] & 3u), (int32_t)(e_m[1] & 3u), (int32_t)(e_m[2] & 3u)};   // u32
+        const int32_t sh_p[3] = {(int32_t)(e_m[0] & 7u), (int32_t)(e_m[1] & 7u), (int32_t)(e_m[2] & 7u)};   // u16
+        const int32_t sh_o[3] = {(int32_t)((uint32_t)(rr0 + rstart[0]) & 3u), (int32_t)((uint32_t)(rr0 + rstart[1]) & 3u),
+                                 (int32_t)((uint32_t)(rr0 + rstart[2]) & 3u)};
+        const int32_t sh_r = (int32_t)((uint32_t)rr0 & 3u);
         // A warp owns RPWB = 4 CONSECUTIVE rows of the band.  Ids are k-major (reading Q4) and the
         // scan offsets are in row order, so the warp's points, quads and CSR entries are each ONE
         // contiguous range: a ROUND takes the next 32 points of that range across row boundaries
@@ -820,6 +821,10 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
             rstart[q + 1] = rstart[q] + (uint32_t)rcnt[q];
         }
         const uint32_t wpts = rstart[RPWB];
+        if (wpts == 0) {   // no points in the warp's rows: nothing else of the band is needed
+            release();
+            continue;
+        }
         // (j, k) of the warp's first row; rows b0+q follow by +q with wrap-around
         const int32_t rf = rr0 + b0;
         const int32_t jf = rf % NV, kf = kA + rf / NV;
