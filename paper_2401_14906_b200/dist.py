@@ -318,6 +318,54 @@ def p2p_transport(group=None):
     return transport
 
 
+def assemble_batched(rank: int, cuts, moves, source, device, group=None):
+    """balance.assemble with the point-to-point traffic in two batches instead of one
+    blocking send / recv per array: (1) every move's stencil-id count, (2) every
+    move's five arrays.  All ranks walk `moves` in the same order, so the posted
+    sends and receives of each rank pair match.  Zero-length arrays are skipped
+    on both sides (their sizes are known to both after batch 1)."""
+    mine = [(k, mv) for k, mv in enumerate(moves) if rank in (mv[0], mv[1])]
+    pieces, cnts, ops = {}, {}, []
+    for k, (s_, d_, g0, g1) in mine:
+        if s_ == rank:
+            pieces[k] = source.piece(g0, g1)
+            cnts[k] = torch.tensor([pieces[k]["stencil_ids"].numel()], dtype=torch.int64, device=device)
+            if d_ != rank:
+                ops.append(dist.P2POp(dist.isend, cnts[k], d_, group))
+        else:
+            cnts[k] = torch.empty(1, dtype=torch.int64, device=device)
+            ops.append(dist.P2POp(dist.irecv, cnts[k], s_, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    ops, parts = [], []
+    keys = ("face_masks", "stencil_offsets", "stencil_ids", "points", "end_offset")
+    for k, (s_, d_, g0, g1) in mine:
+        if s_ == rank and d_ == rank:
+            parts.append((g0, g1, pieces[k]))
+            continue
+        n, c = g1 - g0, int(cnts[k].item())
+        if s_ == rank:
+            for key in keys:
+                t = pieces[k][key].contiguous()
+                if t.numel():
+                    ops.append(dist.P2POp(dist.isend, t, d_, group))
+        else:
+            like = dict(face_masks=torch.empty(n, dtype=torch.uint8, device=device),
+                        stencil_offsets=torch.empty(n, dtype=torch.int32, device=device),
+                        stencil_ids=torch.empty(c, dtype=torch.int32, device=device),
+                        points=torch.empty((n, 3), dtype=torch.float32, device=device),
+                        end_offset=torch.empty(1, dtype=torch.int32, device=device))
+            for key in keys:
+                if like[key].numel():
+                    ops.append(dist.P2POp(dist.irecv, like[key], s_, group))
+            parts.append((g0, g1, like))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    return balance._finish(balance.Shard(cuts[rank], cuts[rank + 1]), parts, device)
+
+
 def shard_halo_exchange(buf: torch.Tensor, shard_windows, moves, rank: int, group=None):
     """C2 on re-cut windows: for every halo move (src, dst, g0, g1), src sends its
     window slice of ids [g0, g1) to dst's window slice (batched P2P)."""
@@ -353,7 +401,7 @@ class BalancedSmoother:
         owned_all = [tuple(int(x) for x in allo[2 * r:2 * r + 2].tolist()) for r in range(self.world)]
         self.cuts = balance.balanced_cuts(total_points, self.world)
         moves = balance.plan_moves(owned_all, self.cuts)
-        self.shard = balance.assemble(self.rank, self.cuts, moves, src, p2p_transport(group), dev)
+        self.shard = assemble_batched(self.rank, self.cuts, moves, src, dev, group)
         win = torch.tensor([self.shard.w0, self.shard.w1], dtype=torch.int64, device=dev)
         allw = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
         dist.all_gather_into_tensor(allw, win, group=group)

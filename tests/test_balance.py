@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_2401_14906_b200 import balance
-from paper_2401_14906_b200.dist import partition, p2p_transport, shard_halo_exchange
+from paper_2401_14906_b200.dist import assemble_batched, partition, p2p_transport, shard_halo_exchange
 
 
 def test_cuts_and_moves_cover_ranges():
@@ -79,6 +79,10 @@ def _worker(rank, world, port, q):
         moves = balance.plan_moves(owned, cuts)
         src = _source(m, *owned[rank])
         sh = balance.assemble(rank, cuts, moves, src, p2p_transport(), "cpu")
+        shb = assemble_batched(rank, cuts, moves, src, "cpu")   # the two-batch form BalancedSmoother uses
+        assert (shb.a0, shb.a1, shb.w0, shb.w1) == (sh.a0, sh.a1, sh.w0, sh.w1)
+        for key in ("face_masks", "stencil_offsets", "stencil_ids", "points"):
+            assert torch.equal(getattr(shb, key), getattr(sh, key)), key
         a0, a1 = cuts[rank], cuts[rank + 1]
         assert (sh.a0, sh.a1) == (a0, a1)
         np.testing.assert_array_equal(sh.face_masks.numpy(), m.face_mask[a0:a1])
