@@ -766,13 +766,11 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
             if (b < nbands) b += G;
         }
     }
-    uint32_t par[kBandBufs];
-#pragma unroll
-    for (int i = 0; i < kBandBufs; ++i) par[i] = 0u;
+    uint32_t par = 0u;   // bit b: fill parity of buffer b (a register, not a dynamically indexed array)
     for (int it = 0;; ++it) {
         const int sb = it % kBandBufs;
-        mbar_wait(&bar[sb], par[sb]);
-        par[sb] ^= 1u;
+        mbar_wait(&bar[sb], (par >> sb) & 1u);
+        par ^= 1u << sb;
         const int32_t band = *reinterpret_cast<volatile int32_t *>(&s_band[sb]);
         if (band >= nbands) break;
         auto release = [&]() {   // this warp is done with buffer sb
