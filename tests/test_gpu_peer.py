@@ -75,9 +75,17 @@ def volume():
     return a
 
 
-@pytest.mark.parametrize("G", [2, 3, 5])
-def test_peer_slabs_match_single(G):
+@pytest.mark.parametrize("G,shape", [(2, 0), (3, 0), (5, 0), (3, 1)])
+def test_peer_slabs_match_single(G, shape):
     p = gu.psn()
+    p.set_constraint(shape)   # box, or the sphere (reading Q26)
+    try:
+        _peer_slabs_match_single(p, G)
+    finally:
+        p.set_constraint(0)
+
+
+def _peer_slabs_match_single(p, G):
     a = volume()
     T, lam, d = 7, 0.5, 0.5
     vols, meshes, firsts, total = extract_slabs(p, a, G, (1.0, 1.0, 1.0))
