@@ -10,6 +10,7 @@ and which PAPER.md passage it follows.
 Functions
 ---------
 layer_counts(vol, ...)        per-voxel-layer (P, Q, S)             P:86
+row_trims(vol, ...)           per-grid-row Pass-1 / Pass-2 trims
 extract(vol, ...)             points, quads, pairs, CSR, face masks
 smooth(mesh, ...)             fp64 Jacobi constrained Laplacian      P:64-69 (Eq. 1)
 triangulate(quads, points)    shortest-diagonal split
@@ -55,6 +56,9 @@ def _load():
         lib.oracle_layer_counts.restype = ctypes.c_int
         lib.oracle_layer_counts.argtypes = [vp, ctypes.c_int, i64, i64, i64, i64, i64,
                                             vp, i64, ctypes.c_int, i64, i64, vp, vp, vp]
+        lib.oracle_row_trims.restype = ctypes.c_int
+        lib.oracle_row_trims.argtypes = [vp, ctypes.c_int, i64, i64, i64, i64, i64,
+                                         vp, i64, ctypes.c_int, i64, i64, vp, vp, vp, vp]
         lib.oracle_extract.restype = ctypes.c_int
         lib.oracle_extract.argtypes = [vp, ctypes.c_int, i64, i64, i64, i64, i64,
                                        vp, i64, ctypes.c_int, vp, vp,
@@ -147,6 +151,26 @@ def layer_counts(vol: Volume, k0: int = 0, k1: int | None = None):
     if rc != 0:
         raise ValueError(f"oracle_layer_counts: bad arguments (rc={rc})")
     return P, Q, S
+
+
+def row_trims(vol: Volume, k0: int = 0, k1: int | None = None):
+    """Per grid row E_{j,k} (j < N, k in [k0, k1)): (pass1, final) trims, each int64 [k1-k0, N, 2]
+    holding [xL, xR): Pass 1 from the x-edges only, final after Pass 2's y/z-edges
+    (P:83); empty rows [0, 0)."""
+    lib = _load()
+    M, N, O = vol.dims
+    if k1 is None:
+        k1 = O
+    n = max(k1 - k0, 0) * N
+    a = [np.zeros(n, np.int64) for _ in range(4)]
+    L, nL, anz, keep = _label_args(vol)
+    lab = np.ascontiguousarray(vol.labels)
+    rc = lib.oracle_row_trims(_ptr(lab), lab.dtype.itemsize, M, N, O, vol.z_lo, vol.z_hi,
+                              _ptr(L), nL, anz, k0, k1, *(_ptr(x) for x in a))
+    if rc != 0:
+        raise ValueError(f"oracle_row_trims: bad arguments (rc={rc})")
+    shape = (max(k1 - k0, 0), N)
+    return np.stack([a[0].reshape(shape), a[1].reshape(shape)], -1), np.stack([a[2].reshape(shape), a[3].reshape(shape)], -1)
 
 
 def extract(vol: Volume, k0: int = 0, k1: int | None = None, point_base: int = 0,

@@ -200,6 +200,47 @@ int oracle_layer_counts(const void *labels, int elem_bytes,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Row trims (Pass 1 and Pass 2)                                             */
+/* ------------------------------------------------------------------------ */
+
+/* For every grid row E_{j,k} (j in [0,N), k in [k0,k1)), the computational
+ * trim of PAPER sec 2.3:
+ *   Pass 1: "the x-edges are classified ... and the trim positions
+ *     xL and xR (first and last x-edge intersection)" -- xl1/xr1 = the
+ *     tightest half-open interval [xL, xR) holding every i with X(i,j,k);
+ *   Pass 2: "the y- and z-edges are classified ... and the trim
+ *     positions adjusted" -- xl/xr = the tightest interval holding every i with
+ *     X(i,j,k), Y(i,j,k) (if j+1 < N) or Z(i,j,k) (if k+1 < O).
+ * An empty row gets [0, 0).  Arrays are [k1-k0][N], row r = j + N (k-k0).
+ * Needs slices [k0, min(k1+1, O)).  Returns 0 or -1 on bad arguments. */
+int oracle_row_trims(const void *labels, int elem_bytes,
+                     int64_t M, int64_t N, int64_t O, int64_t z_lo, int64_t z_hi,
+                     const uint32_t *L, int64_t nL, int all_nonzero,
+                     int64_t k0, int64_t k1,
+                     int64_t *xl1, int64_t *xr1, int64_t *xl, int64_t *xr)
+{
+    OVol v = { labels, elem_bytes, M, N, O, z_lo, z_hi, L, nL, all_nonzero };
+    if (o_check_args(&v)) return -1;
+    if (k0 < 0 || k1 > O || k0 > k1) return -1;
+    if (k0 < k1 && (k0 < z_lo || (k1 < O ? k1 + 1 : O) > z_hi)) return -1;
+    for (int64_t k = k0; k < k1; ++k)
+        for (int64_t j = 0; j < N; ++j) {
+            int64_t r = j + N * (k - k0);
+            int64_t a1 = -1, b1 = -1, a = -1, b = -1;   /* first / last intersection, -1 = none */
+            for (int64_t i = 0; i < M; ++i) {
+                int x = i + 1 < M && o_X(&v, i, j, k);
+                int y = j + 1 < N && o_Y(&v, i, j, k);
+                int z = k + 1 < O && o_Z(&v, i, j, k);
+                if (x) { if (a1 < 0) a1 = i; b1 = i; }
+                if (x || y || z) { if (a < 0) a = i; b = i; }
+            }
+            xl1[r] = a1 < 0 ? 0 : a1; xr1[r] = a1 < 0 ? 0 : b1 + 1;
+            xl[r] = a < 0 ? 0 : a;    xr[r] = a < 0 ? 0 : b + 1;
+        }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Extraction                                                                */
 /* ------------------------------------------------------------------------ */
 

@@ -15,7 +15,7 @@ def load():
                 continue
             key, _, rest = line.partition(" ")
             if key == "case":
-                cur = {"name": rest, "sets": [], "rows": []}
+                cur = {"name": rest, "sets": [], "rows": [], "mquads": []}
             elif key == "end":
                 cases[cur["name"]] = cur
                 cur = None
@@ -23,6 +23,8 @@ def load():
                 cur["sets"].append([int(x) for x in rest.split()])
             elif key == "row":
                 cur["rows"].append(rest)
+            elif key == "mquad":
+                cur["mquads"].append(rest)
             else:
                 cur[key] = rest
     return cases

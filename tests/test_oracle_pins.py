@@ -40,6 +40,130 @@ def test_single_point_golden():
     assert set(indep.edge_multiplicity(m.quads).values()) == {2}
 
 
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16, np.uint32])
+def test_single_point_golden_arrays(dtype):
+    """The 3^3 worked case written out array by array (tests/golden/worked_cases.txt,
+    single_point_3_arrays): quads IN ORDER with their pairs, CSR offsets and ids, face masks.
+    Pins the output ORDER (reading Q4: voxel-major, then x<y<z) that the counting pins cannot see."""
+    case = GOLD["single_point_3_arrays"]
+    a = golden_cases.volume(case, dtype)
+    m = extract(a)
+    quads = np.array([[int(x) for x in q.split("|")[0].split()] for q in case["mquads"]], np.uint32)
+    pairs = np.array([[int(x) for x in q.split("|")[1].split()] for q in case["mquads"]], np.uint32)
+    np.testing.assert_array_equal(m.quads, quads)
+    np.testing.assert_array_equal(m.pairs, pairs)
+    np.testing.assert_array_equal(m.csr_off, np.array(case["csr_off"].split(), np.uint32))
+    np.testing.assert_array_equal(m.csr_ids, np.array(case["csr_ids"].split(), np.uint32))
+    np.testing.assert_array_equal(m.face_mask, np.array(case["face_mask"].split(), np.uint8))
+    np.testing.assert_array_equal(m.voxel_idx, np.array([[i, j, k] for k in (0, 1) for j in (0, 1) for i in (0, 1)]))
+
+
+def test_pass1_rows_golden():
+    """S:218-220 Pass-1 row examples: the x-intersections and the trim [xL, xR) of a
+    row.  Each row is embedded as grid row (j=1, k=1) of an M x 3 x 3 volume whose other rows are
+    background: the oracle's Pass-1 trim of that row is the printed one, and its x-quads (owned by
+    voxels (i,1,1)) sit exactly at the printed x-intersections."""
+    for spec in GOLD["pass1_rows"]["rows"]:
+        vals, _, rest = spec.partition("->")
+        xs, _, trim = rest.partition("|")
+        row = [int(x) for x in vals.split()]
+        xint = [int(x) for x in xs.split()]
+        xl, xr = (int(x) for x in trim.split())
+        M = len(row)
+        a = np.zeros((3, 3, M), np.uint16)
+        a[1, 1, :] = row
+        vol = oracle.as_volume(a)
+        p1, fin = oracle.row_trims(vol)
+        assert tuple(p1[1, 1]) == (xl, xr), (spec, p1[1, 1])
+        m = oracle.extract(vol)
+        vi = m.voxel_idx
+        xq = sorted(int(vi[q[2], 0]) for q in m.quads.tolist()
+                    if len({int(vi[v, 0]) for v in q}) == 1 and tuple(vi[q[2], 1:]) == (1, 1))
+        assert xq == xint, (spec, xq)
+        # rows holding no intersection at all have empty trims [0, 0) (S:215)
+        assert tuple(p1[0, 0]) == (0, 0) and tuple(fin[0, 0]) == (0, 0)
+
+
+def _indep_trims(C):
+    """Pass-1 / Pass-2 trims of every grid row written with numpy edge planes (independent of
+    the oracle's loops): [first, last + 1) of the X (resp. X|Y|Z) intersections, [0, 0) if none."""
+    O, N, M = C.shape
+    X = np.zeros(C.shape, bool); Y = np.zeros(C.shape, bool); Z = np.zeros(C.shape, bool)
+    X[:, :, :-1] = C[:, :, 1:] != C[:, :, :-1]
+    Y[:, :-1, :] = C[:, 1:, :] != C[:, :-1, :]
+    Z[:-1, :, :] = C[1:, :, :] != C[:-1, :, :]
+
+    def tr(E):
+        any_ = E.any(-1)
+        first = np.argmax(E, -1)
+        last = M - 1 - np.argmax(E[..., ::-1], -1)
+        return np.stack([np.where(any_, first, 0), np.where(any_, last + 1, 0)], -1)
+    return tr(X), tr(X | Y | Z)
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16, np.uint32])
+def test_row_trims_tight_and_sound(dtype):
+    """Trims: equal to the tightest intervals of the numpy edge planes, Pass-1
+    inside Pass-2, and SOUND: every point-producing voxel of voxel row (j,k) lies in
+    [max(0, minL-1), min(maxR, M-1)) over the four grid rows (j..j+1, k..k+1)."""
+    rng = np.random.default_rng(42)
+    for t in range(60):
+        a = _random_volume(rng, max_dim=11, dtype=dtype)
+        if dtype == np.uint32:
+            a = (a.astype(np.uint64) * 0x10001 + 0x7F000000).astype(np.uint32) * (a != 0)
+        nz = [v for v in np.unique(a).tolist() if v != 0]
+        ls = None if t % 2 == 0 else (nz[:2] or None)
+        vol = oracle.as_volume(a, label_set=ls)
+        p1, fin = oracle.row_trims(vol)
+        e1, ef = _indep_trims(indep.classes(a, ls))
+        np.testing.assert_array_equal(p1, e1)
+        np.testing.assert_array_equal(fin, ef)
+        nonempty = p1[..., 1] > p1[..., 0]
+        assert np.all(fin[nonempty, 0] <= p1[nonempty, 0]) and np.all(fin[nonempty, 1] >= p1[nonempty, 1])
+        m = oracle.extract(vol)
+        O, N, M = a.shape
+        for i, j, k in m.voxel_idx.tolist():
+            rows = [fin[kk, jj] for kk in (k, k + 1) for jj in (j, j + 1) if fin[kk, jj, 1] > fin[kk, jj, 0]]
+            assert rows, "a point in a voxel row whose four grid rows have no intersection"
+            lo = max(0, min(r[0] for r in rows) - 1)
+            hi = min(max(r[1] for r in rows), M - 1)
+            assert lo <= i < hi
+
+
+def _u32_volume(rng, max_dim=10):
+    """u32 labels that agree in their low 16 (and low 8) bits but differ above: a reader that
+    truncated to u16 / u8 would merge them."""
+    a = _random_volume(rng, max_dim=max_dim, nlab=4).astype(np.uint64)
+    hi = np.array([0, 0x00010000, 0x7FFF0000, 0xFFFE0000], np.uint64)
+    return np.where(a == 0, 0, (a & 1) + 0x5 + hi[a]).astype(np.uint32)
+
+
+def test_u32_counting_identities_and_cuberille():
+    """The u32 read path (psn_oracle.c o_raw elem_bytes 4): counting identities and the textbook
+    cuberille surface on u32 volumes whose labels collide in their low bits, incl. label subsets
+    of large values and the largest non-sentinel value 0xFFFFFFFE."""
+    rng = np.random.default_rng(2024)
+    for t in range(40):
+        a = _u32_volume(rng)
+        if t % 4 == 3:
+            a[a.shape[0] // 2, :, : a.shape[2] // 2] = 0xFFFFFFFE
+        vals = [v for v in np.unique(a).tolist() if v != 0]
+        ls = None if t % 2 == 0 or not vals else vals[: max(1, len(vals) // 2)]
+        P, Q, S = oracle.layer_counts(oracle.as_volume(a, label_set=ls))
+        C = indep.classes(a, ls)
+        assert (int(P.sum()), int(Q.sum()), int(S.sum())) == indep.count_identities(C)
+        if t % 2 == 0:
+            m = _check_against_cuberille(a, label_set=ls)
+            # low-bit collisions really occur and really intersect
+            assert set(m.pairs.ravel().tolist()) <= set(np.unique(C).tolist())
+    # two labels equal in the low 16 bits: the interface between them is a surface
+    a = np.zeros((4, 4, 5), np.uint32)
+    a[1:3, 1:3, 1:3] = 0x00010001
+    a[1:3, 1:3, 3] = 0x00000001
+    m = extract(a)
+    assert [tuple(p) for p in m.pairs.tolist()].count((0x00010001, 0x00000001)) == 4
+
+
 @pytest.mark.parametrize("n", [3, 5, 6])
 def test_single_point_any_size(n):
     a = np.zeros((n, n, n), np.uint8)
