@@ -175,16 +175,62 @@ def oracle_sample(cfg: str, n_layers: int, labels_host=None):
     if labels_host is None:
         labels_host = psn_gen.generate_host(spec, z_lo, z_hi)
     vol = oracle.Volume(np.ascontiguousarray(labels_host), (M, N, O), z_lo, tuple(spec.spacing))
-    t0 = time.perf_counter()
-    mesh = oracle.extract(vol, wa, wb)
-    lay = mesh.voxel_idx[:, 2]
-    frozen = (((lay == wa) & (wa < k0)) | ((lay == wb - 1) & (wb > k1))).astype(np.uint8)
-    oracle.smooth(mesh, tuple(spec.spacing), T, lam, d, frozen=frozen)
-    dt = time.perf_counter() - t0
+    with pinned_core0():
+        t0 = time.perf_counter()
+        mesh = oracle.extract(vol, wa, wb)
+        lay = mesh.voxel_idx[:, 2]
+        frozen = (((lay == wa) & (wa < k0)) | ((lay == wb - 1) & (wb > k1))).astype(np.uint8)
+        oracle.smooth(mesh, tuple(spec.spacing), T, lam, d, frozen=frozen)
+        dt = time.perf_counter() - t0
     return dt, M * N * n_layers, (k0, k1), labels_host
 
 
+def host_info():
+    """lscpu model, online CPUs, and the core the oracle is pinned to (SURVEY 8(d) oracle timing)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.strip().lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "pinned_core": 0, "threads_used": 1}
+
+
+class pinned_core0:
+    """Run the (single-threaded) oracle pinned to core 0 (taskset -c 0 equivalent for this thread)."""
+
+    def __enter__(self):
+        try:
+            self.old = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {0})
+        except Exception:
+            self.old = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.old is not None:
+            try:
+                os.sched_setaffinity(0, self.old)
+            except Exception:
+                pass
+
+
 # --------------------------------------------------------------------------- reference arm
+def sample_text(cfg, k0, k1, vox, T, reps=None):
+    r = f", repeated {reps}x" if reps else ""
+    return (f"{cfg} voxel layers [{k0},{k1}) ({vox} voxels){r}: oracle extract + {T}-iteration fp64 smoothing, "
+            f"single thread pinned to core 0 (the same window the reference arm times per step)")
+
+
+def sample_layers(cfg, voxels):
+    import psn_gen
+    spec = psn_gen.config(cfg)
+    return max(1, int(round(voxels / (spec.M * spec.N))))
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -192,9 +238,8 @@ def run_reference(args, rank, world):
     cfg = args.config
     import psn_gen
     spec = psn_gen.config(cfg)
-    M, N = spec.M, spec.N
-    # bounded sample per step: ~2-4 s of single-core oracle work
-    n_layers = max(1, int(round(args.ref_voxels / (M * N))))
+    # bounded sample per step (~1-2 s of single-core oracle work): the same window cpu_baseline times
+    n_layers = sample_layers(cfg, args.ref_voxels)
     labels = None
     times = []
     for s in range(args.warmup + args.steps):
@@ -203,13 +248,14 @@ def run_reference(args, rank, world):
             times.append(dt)
     t = sum(times)
     value = vox * len(times) / t
-    sample = f"{cfg} voxel layers [{k0},{k1}) ({vox} voxels): oracle extract + {psn_gen.SMOOTHING[cfg][0]}-iteration fp64 smoothing"
-    line = {"metric": METRIC, "value": value, "unit": "voxel/s", "n_gpus": world, "steps": args.steps,
+    sample = sample_text(cfg, k0, k1, vox, psn_gen.SMOOTHING[cfg][0])
+    line = {"metric": METRIC, "value": value, "unit": "voxel/s", "n_gpus": max(world, args.gpus), "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u16/f64" if spec.elem_bytes == 2 else "u8/f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOADS[cfg], "sample": sample},
-            "cpu_baseline": {"value": value, "unit": "voxel/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "voxel/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": value, "unit": "voxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -281,6 +327,11 @@ def run_psn(args, rank, world, local_rank):
 
     K = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    # per-pass events recorded by the library between its launches (psn_ctx_set_pass_events)
+    pev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for e4 in pev:
+        for e in e4:
+            e.record(stream)
     L2_BYTES = 126e6
     flush = torch.empty(int(2 * L2_BYTES), dtype=torch.uint8, device=dev) if V * b <= L2_BYTES else None
     barrier()
@@ -293,6 +344,7 @@ def run_psn(args, rank, world, local_rank):
     for s in range(K):
         if flush is not None:   # inputs fit in L2: flush it between timed steps (outside the events)
             flush.zero_()
+        psn.set_pass_events(pev[s])
         ev[s][0].record(stream)
         run_extract()
         ev[s][1].record(stream)
@@ -300,16 +352,18 @@ def run_psn(args, rank, world, local_rank):
         ev[s][2].record(stream)
     torch.cuda.synchronize()
     clk.mark(False)
+    psn.set_pass_events(None)
     barrier()
     time.sleep(0.05)
     clk.__exit__(None, None, None)
     t_ext = sum(e[0].elapsed_time(e[1]) for e in ev) / K    # ms per step
     t_sm = sum(e[1].elapsed_time(e[2]) for e in ev) / K
     t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / K
+    t_pass = [sum(e[i].elapsed_time(e[i + 1]) for e in pev) / K for i in range(3)]   # count, scan, emit
     if world > 1:
-        tt = torch.tensor([t_ext, t_sm, t_step], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_ext, t_sm, t_step, *t_pass], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ext, t_sm, t_step = (float(x) for x in tt.tolist())
+        t_ext, t_sm, t_step, *t_pass = (float(x) for x in tt.tolist())
     clocks = clk.summary()
     if world > 1 and halo_peer:
         (pipe.peer_halo if args.no_balance else pipe.balanced.peer).check()   # no peer wait timed out
@@ -333,6 +387,20 @@ def run_psn(args, rank, world, local_rank):
                     "prep -- divided by T)"}
     if dominant != "k_smooth_v4":
         roof["note"] += "; extraction dominated this config's step, see extract.frac"
+
+    # per-pass roofline (SURVEY 8(d) per-kernel byte budgets, per GPU): counting reads the labels once,
+    # the scan moves 24 B per voxel row, the emission writes the outputs (+ the face masks)
+    nominal = 8000.0
+    R = (N - 1) * (O - 1)
+    out_bytes = 12 * P + 24 * Q + 4 * (P + 1) + 4 * S + P
+    per_pass = {}
+    for name, t_ms, byt, what in (
+            ("k_count3", t_pass[0], V * b, "labels V*b (incl. the scan-header reset)"),
+            ("k_scan", t_pass[1], 24 * R, "24 B per voxel row"),
+            ("k_emit_band", t_pass[2], out_bytes, "outputs 12P + 24Q + 4(P+1) + 4S + P face masks")):
+        gbs = byt / world / (t_ms * 1e-3) / 1e9 if t_ms > 0 else None
+        per_pass[name] = {"ms": t_ms, "bytes": byt / world, "bytes_model": what, "gbs": gbs,
+                          "frac": gbs / peak if gbs else None, "frac_nominal_8tbs": gbs / nominal if gbs else None}
 
     # ---------------------------------------------------------------- e2e through the public host-buffer API
     e2e = None
@@ -366,11 +434,16 @@ def run_psn(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            n_layers = max(1, int(round(args.cpu_voxels / (M * N))))
-            dt, vox, (k0, k1), _ = oracle_sample(cfg, n_layers,
-                                                 labels_host=lambda a, b_: labels[a:b_].cpu().numpy())
-            cpu = {"value": vox / dt, "unit": "voxel/s", "cores": 1, "kind": "oracle",
-                   "sample": f"{cfg} voxel layers [{k0},{k1}) ({vox} voxels, {dt:.1f} s): oracle extract + {T}-iteration fp64 smoothing, single thread"}
+            n_layers = sample_layers(cfg, args.ref_voxels)
+            lab_fn = lambda a, b_: labels[a:b_].cpu().numpy()   # noqa: E731
+            tot, vox_tot, lab_host = 0.0, 0, None
+            reps = 0
+            while reps < 3 or (tot < args.cpu_seconds and reps < 64):   # ~10-30 s of CPU work
+                dt, vox, (k0, k1), lab_host = oracle_sample(cfg, n_layers, labels_host=lab_host if lab_host is not None else lab_fn)
+                tot += dt; vox_tot += vox; reps += 1
+            cpu = {"value": vox_tot / tot, "unit": "voxel/s", "cores": 1, "kind": "oracle",
+                   "sample": sample_text(cfg, k0, k1, vox, T, reps) + f"; {tot:.1f} s total",
+                   "host": host_info()}
         except Exception as e:  # never fail the bench on the baseline leg
             cpu = {"value": None, "unit": "voxel/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
@@ -389,9 +462,11 @@ def run_psn(args, rank, world, local_rank):
                        "l2": ("inputs larger than L2 (%.2f GB labels, %.2f GB smoothing state)" % (V * b / 1e9, P * 28 / 1e9))
                        if V * b > l2 else "inputs fit in L2: L2 flushed (2x L2 written) before every timed step"},
             "counts": {"points": P, "quads": Q, "stencil": S},
-            "extract": {"ms": t_ext, "voxels_per_s": ext_vps, "bytes_alg": b_ext, "gbs": ext_gbs, "frac": ext_gbs / world / peak},
+            "extract": {"ms": t_ext, "voxels_per_s": ext_vps, "bytes_alg": b_ext, "gbs": ext_gbs, "frac": ext_gbs / world / peak,
+                        "frac_nominal_8tbs": ext_gbs / world / nominal},
+            "per_pass": per_pass,
             "smooth": {"ms": t_sm, "pt_iters_per_s": sm_ptit, "bytes_alg_per_iter": b_sm, "gbs": sm_gbs,
-                       "frac": sm_gbs / world / peak},
+                       "frac": sm_gbs / world / peak, "frac_nominal_8tbs": sm_gbs / world / nominal},
             "roofline": roof,
             "gpu_launches": launches * K if world == 1 else None,
             "clocks": clocks,
@@ -414,13 +489,27 @@ def main():
                     help="N > 1: smoothing halo exchange over NCCL point-to-point instead of the kernel's peer pushes")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-voxels", type=float, default=96e6, help="oracle sample size for cpu_baseline (~10-30 s)")
-    ap.add_argument("--ref-voxels", type=float, default=6e6, help="oracle sample size per reference step")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="cpu_baseline: repeat the reference arm's sample window until this much CPU time")
+    ap.add_argument("--ref-voxels", type=float, default=8e6,
+                    help="oracle sample window per reference step (also the cpu_baseline window)")
+    ap.add_argument("--check-launch", action="store_true",
+                    help="bring up the N ranks (NCCL, or gloo without CUDA), check world == --gpus, print and exit")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N`: bring up N ranks through torchrun (one process per GPU)
+        relaunch(args.gpus)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N ranks for --gpus N")
+        sys.exit(2)
+    if args.check_launch:
+        check_launch(rank, world, local_rank)
+        return
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -439,6 +528,46 @@ def main():
         run_reference(args, 0, 1)
     else:
         run_psn(args, 0, 1, 0)
+
+
+def relaunch(n: int):
+    """Re-exec this command under torch.distributed.run with n local ranks (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    log("bench.py: launching", n, "ranks:", " ".join(cmd[1:]))
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def check_launch(rank, world, local_rank):
+    """--check-launch: every rank joins the process group (NCCL on GPUs, gloo otherwise) and
+    all-gathers its rank; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        print(json.dumps({"n_gpus": 1, "ranks": [0], "backend": None}), flush=True)
+        return
+    use_nccl = torch.cuda.is_available() and torch.cuda.device_count() >= world
+    if use_nccl:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = torch.device("cuda", local_rank)
+    else:
+        dist.init_process_group("gloo")
+        dev = torch.device("cpu")
+    try:
+        t = torch.tensor([rank], dtype=torch.int64, device=dev)
+        out = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        if rank == 0:
+            print(json.dumps({"n_gpus": world, "ranks": [int(x.item()) for x in out],
+                              "backend": "nccl" if use_nccl else "gloo"}), flush=True)
+    finally:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

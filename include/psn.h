@@ -206,6 +206,23 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
 psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws, size_t ws_bytes,
                            const float *src, float *dst, float relaxation, float constraint_distance, void *stream);
 
+/*
+ * Per voxel row plan of the last PSN_COUNT on `ws` (Passes 1-3): for
+ * every counted voxel row r = j + (N-1)(k - kA) (kA = own_k0 - 1 if own_k0 > 0,
+ * else own_k0; layers [kA, kB) include the halo layers), copies into caller
+ * device buffers (stream-ordered, no sync):
+ *   counts  uint32[3][R]  points, owned quads, directed stencil entries of the
+ *                         row (halo layers: points only) -- what Pass 4 emits
+ *                         per row ("planned == emitted");
+ *   trims   int32[R][2]   the row's computational trim [xL, xR) in voxel units
+ *                         (P:81): the first and one past the last
+ *                         point-producing voxel; [0, 0) for rows without points.
+ * Either pointer may be NULL.  *rows (if non-NULL) receives R.  PSN_ERR_STATE
+ * if ws holds no COUNT of this volume; PSN_ERR_ARG for bad arguments.
+ */
+psn_status psn_extract_rows(psn_ctx *ctx, const psn_volume *vol, const void *ws, size_t ws_bytes,
+                            uint32_t *counts, int32_t *trims, int64_t *rows, void *stream);
+
 /* Smoothing strategy of psn_smooth (whole volume):
  *   PSN_SMOOTH_PER_ITERATION (default): one launch per Jacobi iteration.
  *   PSN_SMOOTH_WAVEFRONT: G iterations per persistent launch, scheduled as a
@@ -261,6 +278,14 @@ psn_status psn_smooth_finalize(psn_ctx *ctx, const psn_volume *vol, const psn_me
 psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *points, psn_tri tri,
                            uint32_t *tris, void *stream);
 
+/* Per-pass timing (bench.py's per_pass object): with events != NULL (4 cudaEvent_t
+ * created on the context's device, passed as void*), every later psn_extract
+ * records events[0] before the counting pass (incl. its header reset), [1]
+ * between counting and the scan, [2] between the scan and the emission, [3]
+ * after the emission (a COUNT-only call records [0..2], an EMIT-only call [3]);
+ * stream-ordered, no synchronisation.  events == NULL stops the recording. */
+psn_status psn_ctx_set_pass_events(psn_ctx *ctx, void *const *events);
+
 /* Number of kernel launches the last call on this ctx enqueued (bench.py's gpu_launches). */
 int64_t psn_launch_count(const psn_ctx *ctx);
 
@@ -309,15 +334,20 @@ typedef struct {
  * once per iteration with the same `parity` (the caller's dst buffer index).
  * Ranks without points still call it (the step only waits and signals).
  * PSN_ERR_ARG for the conditions of psn_smooth_step, a NULL peer / sig / ctr /
- * err, or a push range outside the own entries. */
+ * err, or a non-empty push range outside the own entries.  A neighbour wait
+ * longer than 5 s sets *err and traps the kernel (the stream then reports a
+ * launch failure) instead of smoothing on with stale halos. */
 psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
                                 size_t ws_bytes, const float *src, float *dst, int parity, float relaxation,
                                 float constraint_distance, psn_peer *peer, void *stream);
 
 /* `iterations` peer steps from the anchors in one call (no per-step host
- * round trip): step t reads buf[(t-1)&1] (nothing at t = 0) and writes
- * buf[t&1] with parity t&1 -- the loop every rank would otherwise run around
- * psn_smooth_step_peer.  The result is in buf[(iterations-1)&1]. */
+ * round trip): with g = peer->iteration on entry, step t uses parity
+ * p = (g+t)&1, reads buf[p^1] (nothing at t = 0) and writes buf[p] -- the loop
+ * every rank would otherwise run around psn_smooth_step_peer.  The result is in
+ * buf[(peer->iteration - 1) & 1] (peer->iteration as updated by the call).
+ * Continuing the parity across calls keeps a later run's first push out of
+ * the buffer a neighbour's previous run ended in. */
 psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
                                size_t ws_bytes, float *buf0, float *buf1, int32_t iterations, float relaxation,
                                float constraint_distance, psn_peer *peer, void *stream);

@@ -392,6 +392,18 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
             const uint32_t P = __reduce_add_sync(kFull, cnt);
             if (lane == 0) { a.cntP[rr] = P; a.cntQ[rr] = rq[i]; a.cntS[rr] = rs[i]; }
             if (P) {
+                // the row's trim [xL, xR): first and last point-producing voxel (P:81, P:124's final
+                // trim in voxel units; rows without points are empty by their zero count)
+                uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+                for (int q = WPL - 1; q >= 0; --q)
+                    if (wv[q]) lo = 32u * (uint32_t)(lane * WPL + q) + (uint32_t)(__ffs(wv[q]) - 1);
+#pragma unroll
+                for (int q = 0; q < WPL; ++q)
+                    if (wv[q]) hi = 32u * (uint32_t)(lane * WPL + q) + (uint32_t)(32 - __clz(wv[q]));
+                lo = __reduce_min_sync(kFull, lo);
+                hi = __reduce_max_sync(kFull, hi);
+                if (lane == 0) a.trim[rr] = make_int2((int)lo, (int)hi);
                 uint32_t incl = cnt;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {

@@ -229,6 +229,15 @@ __global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, cons
     }
 }
 
+// Offset-buffer load: read-only path normally; for the peer step, whose halo entries are written by the
+// neighbours over NVLink while the kernel runs (.nc data must stay unchanged for the kernel's lifetime),
+// a coherent L2 load.
+template <bool PEER>
+__device__ __forceinline__ float4 ld_src(const float4 *p) {
+    if constexpr (PEER) return __ldcg(p);
+    else return __ldg(p);
+}
+
 template <bool PACKED, bool PREF = false, bool PEER = false, bool SPHERE = false>
 __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
@@ -239,7 +248,11 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
             for (int s = 0; s < 2; ++s) {
                 if (!a.peer.side[s].dst) continue;
                 while (ld_acquire_sys64(a.peer.sig + s) < a.peer.g) {
-                    if (globaltimer_ns() - t0 > kPeerTimeoutNs) { atomicExch(a.peer.err, 1u); break; }
+                    if (globaltimer_ns() - t0 > kPeerTimeoutNs) {   // fail loudly: no smoothing on stale halos
+                        atomicExch(a.peer.err, 1u);
+                        __threadfence_system();
+                        __trap();
+                    }
                     __nanosleep(64);
                 }
             }
@@ -276,9 +289,10 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
             nb = nbr_idx(nbw);
         }
         float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f), h0 = o4, h1 = o4, h2 = o4, h3 = o4;
-        if (src) {
-            o4 = __ldg(src + w);
-            h0 = __ldg(src + nb.x); h1 = __ldg(src + nb.y); h2 = __ldg(src + nb.z); h3 = __ldg(src + nb.w);
+        if (src) {   // PEER: coherent (L2) loads -- neighbours store into the halo entries during the kernel
+            o4 = ld_src<PEER>(src + w);
+            h0 = ld_src<PEER>(src + nb.x); h1 = ld_src<PEER>(src + nb.y);
+            h2 = ld_src<PEER>(src + nb.z); h3 = ld_src<PEER>(src + nb.w);
         }
         const float3 o = make_float3(o4.x, o4.y, o4.z);
         float3 mx, px;
@@ -286,8 +300,8 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
         px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
         if (!act) continue;
         if (src && f) {
-            if ((f & 4u) && lane == 0) { const float4 v = __ldg(src + w - 1u); mx = make_float3(v.x, v.y, v.z); }
-            if ((f & 8u) && (lane == 31 || i + 1u >= n)) { const float4 v = __ldg(src + w + 1u); px = make_float3(v.x, v.y, v.z); }
+            if ((f & 4u) && lane == 0) { const float4 v = ld_src<PEER>(src + w - 1u); mx = make_float3(v.x, v.y, v.z); }
+            if ((f & 8u) && (lane == 31 || i + 1u >= n)) { const float4 v = ld_src<PEER>(src + w + 1u); px = make_float3(v.x, v.y, v.z); }
         }
         float3 r;
         if constexpr (SPHERE)   // sphere of radius d*min(s) about the anchor (reading Q26)

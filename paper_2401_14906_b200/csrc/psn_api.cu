@@ -44,6 +44,7 @@ struct psn_ctx {
     int emit_mode = PSN_EMIT_AUTO;            // psn_ctx_set_emission
     int constraint = PSN_CONSTRAINT_BOX;      // psn_ctx_set_constraint
     std::map<void *, void *> ipc_bases;       // psn_ipc_open: returned pointer -> mapped base
+    cudaEvent_t pass_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // psn_ctx_set_pass_events
 };
 
 namespace {
@@ -313,6 +314,16 @@ namespace {
 bool smooth_packed(const psn_ctx *, const psn_volume *vol);   // below, with the smoothing entry points
 }
 
+static void pass_mark(const psn_ctx *ctx, int i, cudaStream_t st) {
+    if (ctx->pass_ev[i]) cudaEventRecord(ctx->pass_ev[i], st);
+}
+
+psn_status psn_ctx_set_pass_events(psn_ctx *ctx, void *const *events) {
+    if (!ctx) return PSN_ERR_ARG;
+    for (int i = 0; i < 4; ++i) ctx->pass_ev[i] = events ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+    return PSN_OK;
+}
+
 psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *labels, psn_mesh *mesh,
                        unsigned phase, void *ws, size_t ws_bytes, void *stream) {
     if (!ctx) return PSN_ERR_ARG;
@@ -334,6 +345,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     const void *slab0 = vol->labels;   // pointer to slice z_lo
 
     if (phase & PSN_COUNT) {
+        pass_mark(ctx, 0, st);
         if (cudaMemsetAsync(at<char>(ws, L.hdr), 0, L.cntP - L.hdr, st) != cudaSuccess) return cuda_check(ctx, "memset");
         const int64_t E = 16 / eb;                            // elements per 16-byte lane chunk
         const int64_t chunks = (L.M - 1 + E - 1) / E;        // lane chunks per row
@@ -412,6 +424,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
                 ++ctx->launches;
             }
         }
+        pass_mark(ctx, 1, st);
         ScanArgs sa;
         sa.cntP = ca.cntP; sa.cntQ = ca.cntQ; sa.cntS = ca.cntS;
         sa.offP = at<uint32_t>(ws, L.offP); sa.offQ = at<uint32_t>(ws, L.offQ); sa.offS = at<uint32_t>(ws, L.offS);
@@ -421,6 +434,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         sa.tiles = at<TileStatus>(ws, L.tiles); sa.hdr = at<ScanHeader>(ws, L.hdr);
         k_scan<<<(unsigned)L.nTiles, kScanThreads, 0, st>>>(sa);
         ++ctx->launches;
+        pass_mark(ctx, 2, st);
         if ((s = cuda_check(ctx, "count/scan launch")) != PSN_OK) return s;
         ctx->counted[ws] = signature(vol);
         if (!(phase & PSN_EMIT)) return read_totals(ctx, vol, L, ws, mesh, st, nullptr);
@@ -490,7 +504,41 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st, emode);
     else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st, emode);
     ++ctx->launches;
+    pass_mark(ctx, 3, st);
     return cuda_check(ctx, "emit launch");
+}
+
+namespace {
+__global__ void k_rows_out(const uint32_t *cp, const uint32_t *cq, const uint32_t *cs, const int2 *trim, int64_t R,
+                           uint32_t *counts, int2 *trims) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = cp[r];
+        if (counts) { counts[r] = p; counts[R + r] = cq[r]; counts[2 * R + r] = cs[r]; }
+        if (trims) trims[r] = p ? trim[r] : make_int2(0, 0);
+    }
+}
+}  // namespace
+
+psn_status psn_extract_rows(psn_ctx *ctx, const psn_volume *vol, const void *ws, size_t ws_bytes, uint32_t *counts,
+                            int32_t *trims, int64_t *rows, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    Layout L;
+    psn_status s = layout(ctx, vol, &L);
+    if (s != PSN_OK) return s;
+    if (!ws || ws_bytes < L.total) return fail(ctx, PSN_ERR_ARG, "workspace too small: need %zu bytes", L.total);
+    if ((reinterpret_cast<uintptr_t>(trims) & 7u)) return fail(ctx, PSN_ERR_ARG, "trims must be 8-byte aligned");
+    auto it = ctx->counted.find(ws);
+    if (it == ctx->counted.end() || it->second != signature(vol))
+        return fail(ctx, PSN_ERR_STATE, "no PSN_COUNT of this volume on this workspace");
+    if (rows) *rows = L.R;
+    if (!counts && !trims) return PSN_OK;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8));
+    k_rows_out<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        at<uint32_t>(const_cast<void *>(ws), L.cntP), at<uint32_t>(const_cast<void *>(ws), L.cntQ),
+        at<uint32_t>(const_cast<void *>(ws), L.cntS), at<int2>(const_cast<void *>(ws), L.trim), L.R, counts,
+        reinterpret_cast<int2 *>(trims));
+    return cuda_check(ctx, "rows launch");
 }
 
 psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, const void *ws, size_t ws_bytes,
@@ -799,7 +847,10 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
         const psn_peer_side &ps = peer->side[k];
         PeerSide &o = v.peer.side[k];
         if (!ps.dst[0]) continue;
-        if (!ps.dst[1] || !ps.peer_sig || ps.src_begin < own0 || ps.src_end > own1 || ps.src_begin > ps.src_end ||
+        // an empty push range (a rank that only receives on this side, e.g. its first own layer holds no
+        // points) may carry any indices; only a non-empty range must lie inside the own entries
+        if (!ps.dst[1] || !ps.peer_sig || ps.src_begin > ps.src_end ||
+            (ps.src_end > ps.src_begin && (ps.src_begin < own0 || ps.src_end > own1)) ||
             ps.dst_begin < 0 || ((reinterpret_cast<uintptr_t>(ps.dst[parity])) & 15u))
             return fail(ctx, PSN_ERR_ARG, "peer side %d: bad buffers or push range", k);
         o.dst = reinterpret_cast<float4 *>(ps.dst[parity]);
@@ -825,11 +876,16 @@ psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_me
                                float constraint_distance, psn_peer *peer, void *stream) {
     if (!ctx) return PSN_ERR_ARG;
     if (iterations < 0) return fail(ctx, PSN_ERR_ARG, "iterations must be >= 0");
+    if (!peer) return fail(ctx, PSN_ERR_ARG, "peer descriptor is NULL");
     int64_t launches = 0;
     float *buf[2] = {buf0, buf1};
+    // buffer parity continues from the global iteration (not from 0 per call): the first step of a later
+    // run then writes the buffer the neighbour's previous run did NOT end in (the one its finalize reads)
+    const uint64_t g0 = peer->iteration;
     for (int32_t t = 0; t < iterations; ++t) {
-        const psn_status s = psn_smooth_step_peer(ctx, vol, mesh, ws, ws_bytes, t ? buf[(t - 1) & 1] : nullptr,
-                                                  buf[t & 1], t & 1, relaxation, constraint_distance, peer, stream);
+        const int par = (int)((g0 + (uint64_t)t) & 1u);
+        const psn_status s = psn_smooth_step_peer(ctx, vol, mesh, ws, ws_bytes, t ? buf[par ^ 1] : nullptr,
+                                                  buf[par], par, relaxation, constraint_distance, peer, stream);
         if (s != PSN_OK) return s;
         launches += ctx->launches;
     }

@@ -100,6 +100,9 @@ def lib():
         L.psn_extract.restype = ctypes.c_int
         L.psn_mesh_totals.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_mesh_totals.restype = ctypes.c_int
+        L.psn_extract_rows.argtypes = [vp, ctypes.POINTER(Volume), vp, ctypes.c_size_t, vp, vp,
+                                       ctypes.POINTER(ctypes.c_int64), vp]
+        L.psn_extract_rows.restype = ctypes.c_int
         L.psn_smooth_workspace.argtypes = [ctypes.POINTER(MeshC), ctypes.POINTER(ctypes.c_size_t)]
         L.psn_smooth_workspace.restype = ctypes.c_int
         L.psn_smooth_prepare.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
@@ -125,6 +128,8 @@ def lib():
         L.psn_ctx_set_counting.restype = ctypes.c_int
         L.psn_smooth_status.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_smooth_status.restype = ctypes.c_int
+        L.psn_ctx_set_pass_events.argtypes = [vp, ctypes.POINTER(vp)]
+        L.psn_ctx_set_pass_events.restype = ctypes.c_int
         L.psn_launch_count.argtypes = [vp]
         L.psn_launch_count.restype = i64
         if hasattr(L, "psn_smooth_step_peer"):   # (absent from older builds loaded via PSN_LIB)
@@ -147,9 +152,9 @@ def lib():
 
 
 EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
-            "psn_extract_workspace", "psn_extract", "psn_mesh_totals", "psn_smooth_workspace",
+            "psn_extract_workspace", "psn_extract", "psn_extract_rows", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
-            "psn_ctx_set_smoothing", "psn_smooth_status", "psn_ctx_set_counting",
+            "psn_ctx_set_smoothing", "psn_ctx_set_pass_events", "psn_smooth_status", "psn_ctx_set_counting",
             "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_smooth_run_peer", "psn_ipc_export",
             "psn_ipc_open", "psn_ipc_close"]
 
@@ -334,6 +339,19 @@ class PSN:
         self._check(rc)
         return mesh
 
+    def rows(self, vol: Volume, ws: torch.Tensor, stream=None):
+        """psn_extract_rows: per voxel row (counts int32 [3, R] = P/Q/S, trims int32 [R, 2] = [xL, xR))
+        of the last PSN_COUNT on ws (uint32 values in int32 tensors)."""
+        R = ctypes.c_int64()
+        self._check(self.L.psn_extract_rows(self.h, ctypes.byref(vol), _ptr(ws), ws.numel(), None, None,
+                                            ctypes.byref(R), _stream(stream)))
+        dev = ws.device
+        counts = torch.empty((3, max(R.value, 1)), dtype=torch.int32, device=dev)
+        trims = torch.empty((max(R.value, 1), 2), dtype=torch.int32, device=dev)
+        self._check(self.L.psn_extract_rows(self.h, ctypes.byref(vol), _ptr(ws), ws.numel(), _ptr(counts),
+                                            _ptr(trims), None, _stream(stream)))
+        return counts[:, :R.value], trims[:R.value]
+
     # ------------------------------------------------------------------ smoothing / triangulation
     def smooth_workspace(self, mesh: Mesh) -> torch.Tensor:
         n = ctypes.c_size_t()
@@ -354,6 +372,21 @@ class PSN:
     def set_smoothing(self, mode: int = 1, iterations_per_launch: int = 0, points_per_tile: int = 0):
         """1 = one launch per iteration (default), 0 = wavefront (temporally blocked)."""
         self._check(self.L.psn_ctx_set_smoothing(self.h, int(mode), int(iterations_per_launch), int(points_per_tile)))
+
+    def set_pass_events(self, events=None):
+        """Record 4 torch.cuda.Events around the passes of every later psn_extract (None: stop):
+        [0] before counting, [1] counting -> scan, [2] scan -> emission, [3] after emission."""
+        if events is None:
+            self._check(self.L.psn_ctx_set_pass_events(self.h, None))
+            self._pass_events = None
+            return
+        assert len(events) == 4
+        for e in events:   # torch creates the CUDA event lazily: force it (once)
+            if not e.cuda_event:
+                e.record()
+        arr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+        self._pass_events = (events, arr)
+        self._check(self.L.psn_ctx_set_pass_events(self.h, arr))
 
     def set_counting(self, mode: int = 0):
         """0 = automatic (warp-per-row k_count3 when a row fits a warp), 1 = x-tiled k_count."""
@@ -402,7 +435,7 @@ class PSN:
                                         _ptr(bufs[0]), _ptr(bufs[1]), int(iterations), float(relaxation),
                                         float(constraint), ctypes.byref(peer), _stream(stream))
         self._check(rc)
-        return bufs[(iterations - 1) & 1] if iterations else None
+        return bufs[(peer.iteration - 1) & 1] if iterations else None
 
     def ipc_export(self, t: torch.Tensor) -> bytes:
         """CUDA IPC handle (+ offset) of tensor t's memory, as bytes for the peer processes."""

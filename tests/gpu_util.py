@@ -47,3 +47,45 @@ def assert_mesh_equal(g, om, window_lo=0):
     np.testing.assert_array_equal(g["csr_off"], om.csr_off)
     np.testing.assert_array_equal(g["csr_ids"], om.csr_ids)
     np.testing.assert_array_equal(g["face_mask"], om.face_mask)
+
+
+def oracle_rows(om, dims, k0=0, k1=None):
+    """Per voxel row (layers [k0, k1), r = j + (N-1)(k - k0)) of an oracle mesh: P/Q/S counts and the
+    tight point range [min i, max i + 1) ([0, 0) without points)."""
+    M, N, O = dims
+    k1 = O - 1 if k1 is None else k1
+    R = (N - 1) * (k1 - k0)
+    vi = om.voxel_idx
+    r = vi[:, 1] + (N - 1) * (vi[:, 2] - k0)
+    deg = np.diff(om.csr_off.astype(np.int64))
+    P = np.bincount(r, minlength=R)
+    Q = np.bincount(r[om.quads[:, 2].astype(np.int64) - om.point_base], minlength=R) if om.n_quads else np.zeros(R, np.int64)
+    S = np.bincount(r, weights=deg, minlength=R).astype(np.int64)
+    lo = np.zeros(R, np.int64); hi = np.zeros(R, np.int64)
+    if om.n_points:
+        starts = np.flatnonzero(np.r_[True, r[1:] != r[:-1]])
+        rows = r[starts]
+        lo[rows] = np.minimum.reduceat(vi[:, 0], starts)
+        hi[rows] = np.maximum.reduceat(vi[:, 0], starts) + 1
+    return np.stack([P, Q, S]), np.stack([lo, hi], -1)
+
+
+def check_rows(g_counts, g_trims, om, ovol, k0=0, k1=None):
+    """S:602 planned per-row counts == emitted per-row counts (the oracle's), and the GPU's trims
+    are the tight point ranges, inside the paper's voxel-row range from the oracle's Pass-2 grid-row
+    trims ([max(0, minL-1), min(maxR, M-1)) over grid rows (j..j+1, k..k+1))."""
+    M, N, O = ovol.dims
+    k1 = O - 1 if k1 is None else k1
+    cnt, tr = oracle_rows(om, ovol.dims, k0, k1)
+    np.testing.assert_array_equal(g_counts.astype(np.int64), cnt)
+    np.testing.assert_array_equal(g_trims.astype(np.int64), tr)
+    _, fin = oracle.row_trims(ovol, k0, k1 + 1)            # grid rows of slices [k0, k1]
+    has = fin[..., 1] > fin[..., 0]
+    big = np.iinfo(np.int64).max
+    lo4 = np.where(has, fin[..., 0], big)
+    hi4 = np.where(has, fin[..., 1], -1)
+    minL = np.minimum.reduce([lo4[:-1, :-1], lo4[:-1, 1:], lo4[1:, :-1], lo4[1:, 1:]]).reshape(-1)
+    maxR = np.maximum.reduce([hi4[:-1, :-1], hi4[:-1, 1:], hi4[1:, :-1], hi4[1:, 1:]]).reshape(-1)
+    pts = cnt[0] > 0
+    assert np.all(tr[pts, 0] >= np.maximum(0, minL[pts] - 1))
+    assert np.all(tr[pts, 1] <= np.minimum(maxR[pts], M - 1))

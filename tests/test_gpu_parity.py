@@ -58,6 +58,9 @@ def _check_volume(a, label_set=None, spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 
     g = gu.mesh_np(mesh)
     assert (mesh.n_points, mesh.n_quads, mesh.n_stencil) == (om.n_points, om.n_quads, om.n_stencil)
     gu.assert_mesh_equal(g, om)
+    counts, trims = p.rows(vol, mesh.ws)
+    gu.check_rows(counts.cpu().numpy().view(np.uint32), trims.cpu().numpy(), om,
+                  oracle.as_volume(a, spacing, origin, label_set))
     if om.n_points:
         pts = p.smooth(vol, mesh, T, 0.5, 0.5)
         ref = oracle.smooth(om, spacing, T, 0.5, 0.5)
@@ -132,6 +135,8 @@ def test_config_full(name):
     mesh = p.extract(vol)
     om = oracle.extract(oracle.as_volume(host, sp))
     gu.assert_mesh_equal(gu.mesh_np(mesh), om)
+    counts, trims = p.rows(vol, mesh.ws)
+    gu.check_rows(counts.cpu().numpy().view(np.uint32), trims.cpu().numpy(), om, oracle.as_volume(host, sp))
     pts = p.smooth(vol, mesh, T, lam, d)
     ref = oracle.smooth(om, sp, T, lam, d)
     gp = pts[:om.n_points].cpu().numpy()

@@ -138,6 +138,41 @@ def test_peer_balanced_shards_match_single(G):
     np.testing.assert_array_equal(got, s1[:m1.n_points].cpu().numpy())
 
 
+def test_peer_slab_cut_above_flat_top_face():
+    """A slab cut directly above an object's flat top face: rank 1's first own layer holds no
+    points while rank 0's last one does, so rank 1 only RECEIVES on its lower side (peer_sides
+    gives it the empty push (0, 0, 0) with a non-zero halo) -- accepted, signalled, bit-exact."""
+    from paper_2401_14906_b200.dist import partition
+    p = gu.psn()
+    O, N, M = 20, 12, 14
+    k0 = partition(O - 1, 2)[1][0]
+    a = np.zeros((O, N, M), np.uint16)
+    a[3:k0, 2:N - 2, 2:M - 3] = 3          # top face in lattice slice k0-1: voxel layer k0-1 has points, k0 none
+    a[5:k0, 4:6, 4:6] = 5
+    vols, meshes, firsts, total = extract_slabs(p, a, 2, (1.0, 1.0, 1.0))
+    table = torch.tensor([[m.n_points, m.n_quads, m.n_stencil, m.c.halo_lo_points, m.c.halo_hi_points]
+                          for m in meshes])
+    assert meshes[1].c.halo_lo_points > 0
+    sends = slab_sends(table)
+    lower, _ = peer_sides(1, 2, sends)
+    assert lower is not None and lower[1] <= lower[0]     # rank 1 pushes nothing down
+    T, lam, d = 5, 0.5, 0.5
+    sws = [p.smooth_workspace(m) for m in meshes]
+    for r in range(2):
+        p.smooth_prepare(vols[r], meshes[r], sws[r])
+    bufs = [[p.offsets_buffer(m.n_window, "cuda") for _ in range(2)] for m in meshes]
+    src = peer_loop(p, vols, meshes, sws, bufs, sends, 2, T, lam, d)
+    outs = []
+    for r in range(2):
+        out = torch.empty((max(meshes[r].n_window, 1), 3), dtype=torch.float32, device="cuda")
+        p.smooth_finalize(vols[r], meshes[r], src[r], out)
+        outs.append(out)
+    g = concat(meshes, outs)
+    _, vol1, m1, _ = gu.gpu_extract(a)
+    s1 = p.smooth(vol1, m1, T, lam, d)
+    np.testing.assert_array_equal(g["smoothed"], s1[:m1.n_points].cpu().numpy())
+
+
 def test_peer_step_argument_errors():
     from paper_2401_14906_b200.psn import PSNError, PSN_ERR_ARG
     p = gu.psn()
@@ -222,10 +257,16 @@ def test_run_peer_single_rank_matches_single():
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     pr = Peer()
     pr.sig, pr.ctr, pr.err = sig.data_ptr(), ctr.data_ptr(), err.data_ptr()
-    res = p.smooth_run_peer(vols[0], meshes[0], ws, bufs, T, lam, d, pr)
-    out = torch.empty((meshes[0].n_window, 3), dtype=torch.float32, device="cuda")
-    p.smooth_finalize(vols[0], meshes[0], res, out)
     _, vol1, m1, _ = gu.gpu_extract(a)
     s1 = p.smooth(vol1, m1, T, lam, d)
-    np.testing.assert_array_equal(out[:m1.n_points].cpu().numpy(), s1[:m1.n_points].cpu().numpy())
-    assert pr.iteration == T and int(err.item()) == 0
+    # two runs back to back (T odd the second time): the buffer parity continues from the global
+    # iteration, and each run's result (in bufs[(iteration - 1) & 1]) equals psn_smooth
+    for run, TT in enumerate((T, T - 1)):
+        s1 = p.smooth(vol1, m1, TT, lam, d)
+        g0 = pr.iteration
+        res = p.smooth_run_peer(vols[0], meshes[0], ws, bufs, TT, lam, d, pr)
+        assert res is bufs[(g0 + TT - 1) & 1]
+        out = torch.empty((meshes[0].n_window, 3), dtype=torch.float32, device="cuda")
+        p.smooth_finalize(vols[0], meshes[0], res, out)
+        np.testing.assert_array_equal(out[:m1.n_points].cpu().numpy(), s1[:m1.n_points].cpu().numpy())
+    assert pr.iteration == 2 * T - 1 and int(err.item()) == 0
