@@ -141,7 +141,7 @@ psn_status psn_extract_workspace(const psn_volume *vol, size_t *bytes);
  *       psn_ctx_set_counting), then the row-wise exclusive scan (k_scan).  Reads 3 totals back (one stream synchronisation) into
  *       mesh->n_points/n_quads/n_stencil/halo_*.  PSN_ERR_OVERFLOW if any total
  *       reaches 2^32.
- *   phase == PSN_EMIT: Pass 4 (k_emit_band / k_emit_row / k_emit_fast / k_emit,
+ *   phase == PSN_EMIT: Pass 4 (k_emit_band / k_emit_fast / k_emit,
  *       psn_ctx_set_emission) into the caller's arrays, using the
  *       scan kept in `ws` by the preceding PSN_COUNT.  Capacities are checked on
  *       the host against the counted totals (PSN_ERR_CAPACITY, nothing launched).
@@ -253,12 +253,12 @@ psn_status psn_ctx_set_constraint(psn_ctx *ctx, int shape);
 
 /* Emission kernel of psn_extract(PSN_EMIT) (Pass 4):
  *   PSN_EMIT_AUTO (default): band-staged k_emit_band (TMA-staged point planes,
- *     warp-per-row emission) when a row has <= 32 point-plane words (M <= 1025);
- *   PSN_EMIT_ROW: k_emit_row (row metadata pipelined one row ahead), same limit;
+ *     4 rows per warp) when a row has <= 32 point-plane words (M <= 1025);
  *   PSN_EMIT_SCAN: the general k_emit (per-row packed prefix scans, any width).
  * Wider rows always use the row-prefix / scan kernels.  All produce identical
- * outputs (tested). */
-enum { PSN_EMIT_AUTO = 0, PSN_EMIT_ROW = 1, PSN_EMIT_SCAN = 2 };
+ * outputs (tested).  (Mode 1, the former row-pipelined kernel, was removed:
+ * PSN_ERR_ARG.) */
+enum { PSN_EMIT_AUTO = 0, PSN_EMIT_SCAN = 2 };
 psn_status psn_ctx_set_emission(psn_ctx *ctx, int mode);
 
 /* Synchronising check of the last psn_smooth on ws: PSN_ERR_CUDA if a

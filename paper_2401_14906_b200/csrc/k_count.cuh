@@ -45,6 +45,7 @@ struct CountArgs {
     int64_t nXT, nJB, KZ;      // grid decomposition
     int64_t RB;                // bytes per staged row buffer (multiple of 16)
     uint32_t *cntP, *cntQ, *cntS;
+    uint32_t *cntYZ;           // k_count3: per row y | z << 16 face counts (k_scan completes S with them)
     int2 *trim;
     uint32_t *pmask;
     uint16_t *ppre;            // per pmask word: points before it within the CTA's x-tile

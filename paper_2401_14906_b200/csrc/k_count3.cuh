@@ -132,12 +132,22 @@ __device__ __forceinline__ uint32_t movemask(uint32_t w) {
 }
 
 // Slow path of one voxel-row chunk: A/B = grid rows j/j+1 of slice k, C/D of
-// slice k+1 (shared addresses of the chunk).  Returns the E point bits and
-// adds the owned quads (open boundaries P:264) and directed stencil
-// entries of the chunk's voxels to cq / cs.
+// slice k+1 (shared addresses of the chunk).  Returns the E point bits; adds the
+// owned quads (open boundaries P:264) to cq and the chunk's FACE counts to
+// cs, packed x | y << 10 | z << 20 (each <= E per chunk):
+//   x: -x faces of the row's voxels (between voxels i-1 and i, both existing) whose
+//      four corners are not all one class -- each is TWO stencil entries of
+//      this row (voxel i's -x, voxel i-1's +x);
+//   y: -y faces (rows j-1 / j, j >= 1) -- one entry of this row and one of row j-1;
+//   z: -z faces (layers k-1 / k, k >= 1) -- one entry of this row and one of layer k-1.
+// A face is shared by its two voxels, so each is evaluated once: the row's
+// directed stencil count is S = 2x + y + z + y(row j+1) + z(layer k+1), the last
+// two added by the scan (k_scan, ScanArgs.cntYZ).  The point bit is "some corner
+// differs from corner A" (c^e != 0): the union of the three -faces' corner
+// sets plus corner D1.
 struct SlowCtx {
     int64_t M;
-    uint32_t mz, my, mpy, mpz;   // MSB masks of the warp-uniform face conditions (k>=1, j>=1, j<=N-3, k<=O-3)
+    uint32_t mz, my;             // flag masks of the warp-uniform face conditions (k>=1, j>=1)
     uint32_t mqx, mqy, mqz;      // owned-quad conditions (j>=1&&k>=1, k>=1, j>=1)
     bool own;
 };
@@ -159,54 +169,45 @@ __device__ __forceinline__ uint32_t slow_chunk(uint32_t aA, uint32_t aB, uint32_
     uint32_t hA[NW], hB[NW], hC[NW], hD[NW];
     shift1<T>(A, nA, hA); shift1<T>(B, nB, hB); shift1<T>(C, nC, hC); shift1<T>(D, nD, hD);
     // voxel-validity masks: interior chunks (the common case) need no per-element work
-    uint32_t mvox[NW], mi1[NW], miM3[NW];
-    if (xc >= 1 && (int64_t)xc + E + 2 <= sc.M) {
+    uint32_t mvox[NW], mi1[NW];
+    if (xc >= 1 && (int64_t)xc + E + 1 <= sc.M) {
 #pragma unroll
-        for (int q = 0; q < NW; ++q) { mvox[q] = FL; mi1[q] = FL; miM3[q] = FL; }
+        for (int q = 0; q < NW; ++q) { mvox[q] = FL; mi1[q] = FL; }
     } else {
 #pragma unroll
-        for (int q = 0; q < NW; ++q) { mvox[q] = 0; mi1[q] = 0; miM3[q] = 0; }
+        for (int q = 0; q < NW; ++q) { mvox[q] = 0; mi1[q] = 0; }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const uint32_t bit = 1u << ((EB * (e % EPW) + Flags<T>::POS0) & 31);
             const int64_t i = xc + e;
             if (i <= sc.M - 2) mvox[e / EPW] |= bit;
-            if (i >= 1) mi1[e / EPW] |= bit;
-            if (i <= sc.M - 3) miM3[e / EPW] |= bit;
+            if (i >= 1 && i <= sc.M - 2) mi1[e / EPW] |= bit;
         }
     }
-    uint32_t bits = 0, qacc = 0, sacc = 0;
+    uint32_t bits = 0, qacc = 0, fxc = 0, fyc = 0, fzc = 0;
 #pragma unroll
     for (int q = 0; q < NW; ++q) {
-        const uint32_t a = A[q], b = B[q], c = C[q], d = D[q], ha = hA[q], hb = hB[q], hc = hC[q], hd = hD[q];
+        const uint32_t a = A[q], b = B[q], c = C[q], ha = hA[q];
         const uint32_t xa = a ^ ha, yab = a ^ b, zac = a ^ c;
-        const uint32_t Fmx = nz<T>(yab | zac | (a ^ d));          // face x=i   : corners A B C D
-        const uint32_t Fpx = nz<T>((ha ^ hb) | (ha ^ hc) | (ha ^ hd));
-        const uint32_t Fmy = nz<T>(xa | zac | (a ^ hc));          // face y=j   : A hA C hC
-        const uint32_t Fpy = nz<T>((b ^ hb) | (b ^ d) | (b ^ hd));
-        const uint32_t Fmz = nz<T>(xa | yab | (a ^ hb));          // face z=k   : A hA B hB
-        const uint32_t Fpz = nz<T>((c ^ hc) | (c ^ d) | (c ^ hd));
-        const uint32_t pt = (Fmx | Fpx | Fmy | Fpy) & mvox[q];    // each edge lies on one of these faces
+        const uint32_t fx = yab | zac | (a ^ D[q]);     // face x=i : corners A B C D
+        const uint32_t fy = xa | zac | (a ^ hC[q]);     // face y=j : A hA C hC
+        const uint32_t fz = xa | yab | (a ^ hB[q]);     // face z=k : A hA B hB
+        const uint32_t mv = mvox[q];
+        const uint32_t pt = nz<T>(fx | fy | fz | (a ^ hD[q])) & mv;   // the 8 corners are not all one class
         bits |= movemask<T>(pt) << (q * EPW);
+        fyc += __popc(nz<T>(fy) & mv & sc.my);
+        fzc += __popc(nz<T>(fz) & mv & sc.mz);
         if (sc.own) {
-            const uint32_t mv = mvox[q];
-            // directed stencil entries: faces whose neighbour voxel exists
-            uint32_t s = Fmz & mv & sc.mz;
-            s = pack<T>(s, Fmy & mv & sc.my);
-            s = pack<T>(s, Fmx & mv & mi1[q]);
-            s = pack<T>(s, Fpx & miM3[q]);
-            s = pack<T>(s, Fpy & mv & sc.mpy);
-            s = pack<T>(s, Fpz & mv & sc.mpz);
-            sacc += __popc(s);
+            fxc += __popc(nz<T>(fx) & mi1[q]);
             // owned quads: x at (j>=1, k>=1), y at (i>=1, k>=1), z at (i>=1, j>=1)
             uint32_t u = nz<T>(xa) & mv & sc.mqx;
-            u = pack<T>(u, nz<T>(yab) & mv & mi1[q] & sc.mqy);
-            u = pack<T>(u, nz<T>(zac) & mv & mi1[q] & sc.mqz);
+            u = pack<T>(u, nz<T>(yab) & mi1[q] & sc.mqy);
+            u = pack<T>(u, nz<T>(zac) & mi1[q] & sc.mqz);
             qacc += __popc(u);
         }
     }
     cq += qacc;
-    cs += sacc;
+    cs += fxc | (fyc << 10) | (fzc << 20);
     return bits;
 }
 
@@ -325,13 +326,12 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
         sc.M = M;
         sc.own = (k >= a.own_k0) && (k < a.own_k1);
         sc.mz = (k >= 1) ? MSB : 0u;
-        sc.mpz = (k <= a.O - 3) ? MSB : 0u;
         sc.mqy = sc.mz;
         const uint32_t a0 = sbase + (uint32_t)slot0 * SB + (uint32_t)r0 * RB;
         const uint32_t a1 = sbase + (uint32_t)slot1 * SB + (uint32_t)r0 * RB;
-        uint32_t rq[RPW], rs[RPW], dirty = 0;
+        uint32_t rq[RPW], rsx[RPW], rsy[RPW], rsz[RPW], dirty = 0;
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) { rq[i] = 0; rs[i] = 0; }
+        for (int i = 0; i < RPW; ++i) { rq[i] = 0; rsx[i] = 0; rsy[i] = 0; rsz[i] = 0; }
         // classify: every non-uniform (row, chunk) of the layer goes to the warp's queue
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
@@ -359,7 +359,6 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                 const int64_t j = jw + ri;
                 SlowCtx sj = sc;
                 sj.my = (j >= 1) ? MSB : 0u;
-                sj.mpy = (j <= N - 3) ? MSB : 0u;
                 sj.mqz = sj.my;
                 sj.mqx = (j >= 1 && k >= 1) ? MSB : 0u;
                 const uint32_t off = (uint32_t)ri * RB + (uint32_t)c * 16u;
@@ -367,12 +366,11 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                                                          ls, cq, cs);
                 if (bits) atomicOr(&wm[r0 + ri][(c * E) >> 5], bits << ((c * E) & 31));
             }
-            if (sc.own) {
 #pragma unroll
-                for (int i = 0; i < RPW; ++i) {
-                    rq[i] += __reduce_add_sync(kFull, ri == i ? cq : 0u);
-                    rs[i] += __reduce_add_sync(kFull, ri == i ? cs : 0u);
-                }
+            for (int i = 0; i < RPW; ++i) {
+                if (sc.own) rq[i] += __reduce_add_sync(kFull, ri == i ? cq : 0u);
+                const uint32_t f = __reduce_add_sync(kFull, ri == i ? cs : 0u);   // <= 32 E per field: no carry
+                rsx[i] += f & 1023u; rsy[i] += (f >> 10) & 1023u; rsz[i] += f >> 20;
             }
         }
         qt = 0;
@@ -383,14 +381,18 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
             if (r0 + i >= nrows) break;
             const int64_t rr = jw + i + NV * (k - a.kA);
             if (!((dirty >> i) & 1u)) {
-                if (lane == 0) { a.cntP[rr] = 0u; a.cntQ[rr] = 0u; a.cntS[rr] = 0u; }
+                if (lane == 0) { a.cntP[rr] = 0u; a.cntQ[rr] = 0u; a.cntS[rr] = 0u; a.cntYZ[rr] = 0u; }
                 continue;
             }
             uint32_t wv[WPL], cnt = 0;
 #pragma unroll
             for (int q = 0; q < WPL; ++q) { wv[q] = wm[r0 + i][lane * WPL + q]; cnt += __popc(wv[q]); }
             const uint32_t P = __reduce_add_sync(kFull, cnt);
-            if (lane == 0) { a.cntP[rr] = P; a.cntQ[rr] = rq[i]; a.cntS[rr] = rs[i]; }
+            if (lane == 0) {   // S without the +y / +z faces (the scan adds rows j+1 / k+1's y / z counts)
+                a.cntP[rr] = P; a.cntQ[rr] = rq[i];
+                a.cntS[rr] = sc.own ? 2u * rsx[i] + rsy[i] + rsz[i] : 0u;
+                a.cntYZ[rr] = rsy[i] | (rsz[i] << 16);
+            }
             if (P) {
                 // the row's trim [xL, xR): first and last point-producing voxel (P:81, P:124's final
                 // trim in voxel units; rows without points are empty by their zero count)

@@ -413,189 +413,6 @@ __global__ void __launch_bounds__(256) k_emit_fast(EmitArgs a) {
         }
     }
 }
-// Pass 4 for rows of at most 32 point-plane words (M <= 1025), the common case.
-// Same outputs as k_emit_fast, organised for memory-level parallelism:
-//   * a warp owns a voxel row; lane w holds word w of the point planes of the
-//     row and of its five neighbour rows (and their per-word prefixes), so a
-//     neighbour id is two shuffles + a popcount -- no dependent global loads
-//     in the per-point phase except the 8 corner labels;
-//   * the next row's metadata (counts, offsets, the 12 plane words per lane)
-//     is loaded while the current row's points are emitted (software
-//     pipelining one row ahead), so a row costs ~one memory round trip.
-struct RowMeta {
-    uint32_t cnt, offP, qbase, sbase, noff;   // noff: lanes 0..4 = neighbour row q's offP
-    uint32_t om, op;                          // own word / prefix at lane w
-    uint32_t nm[5], np[5];                    // neighbour rows' words / prefixes at lane w
-};
-
-template <typename T, bool ANZ>
-__global__ void __launch_bounds__(256) k_emit_row(EmitArgs a) {
-    __shared__ uint32_t sbits[ANZ ? 1 : 2048];
-    __shared__ uint16_t slist[kEmitWarps][1024];      // x of the row's points, by running index
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    LabelSet ls = a.ls;
-    if (!ANZ && sizeof(T) < 4) {
-        for (int t = threadIdx.x; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
-        ls.bits = sbits;
-        __syncthreads();
-    }
-    const uint64_t totP = a.hdr->total[0], totQ = a.hdr->total[1], totS = a.hdr->total[2];
-    const uint32_t halo_lo = (uint32_t)a.hdr->halo_lo;
-    if (totP > (uint64_t)a.cap_points || totQ > (uint64_t)a.cap_quads || totS > (uint64_t)a.cap_stencil) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) a.hdr->emit_status = 1u;
-        return;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const uint64_t before_hi = (a.kB > a.own_k1) ? a.hdr->halo_hi : totP;
-        a.hdr->emit_status = 0u;
-        a.csr_off[before_hi - halo_lo] = a.first_stencil + (uint32_t)totS;   // CSR sentinel entry
-    }
-    const uint32_t gid_base = a.first_point - halo_lo;
-    const uint32_t M = (uint32_t)a.M, N = (uint32_t)a.N, NV = N - 1, W32 = (uint32_t)a.W32;
-    const uint32_t R = (uint32_t)a.R;
-    const uint32_t kA = (uint32_t)a.kA, kB = (uint32_t)a.kB, own0 = (uint32_t)a.own_k0, own1 = (uint32_t)a.own_k1;
-    const T *lab = reinterpret_cast<const T *>(a.labels);
-    const bool wok = (uint32_t)lane < W32;
-
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    uint32_t rr = blockIdx.x * (blockDim.x >> 5) + warp;
-    uint32_t j = rr % NV, k = kA + rr / NV;
-    const uint32_t dj = warps % NV, dk = warps / NV;
-
-    // metadata of row (rr, j, k); loads only (no use), so it overlaps the previous row's work
-    auto fetch = [&](uint32_t r, uint32_t jj, uint32_t kk, RowMeta &m) {
-        m.cnt = r < R ? __ldg(a.cntP + r) : 0u;
-        if (r >= R) return;
-        const bool own = (kk >= own0) && (kk < own1);
-        m.offP = __ldg(a.offP + r);
-        m.qbase = own ? __ldg(a.offQ + r) : 0u;
-        m.sbase = own ? __ldg(a.offS + r) : 0u;
-        m.om = wok ? __ldg(a.pmask + (size_t)r * W32 + lane) : 0u;
-        m.op = wok ? (uint32_t)__ldg(a.ppre + (size_t)r * W32 + lane) : 0u;
-        m.noff = 0u;
-        if (lane < 5 && own) {
-            const bool ok = lane == 0 ? (jj >= 1 && kk >= kA + 1) : lane == 1 ? (kk >= kA + 1)
-                          : lane == 2 ? (jj >= 1) : lane == 3 ? (jj + 1 <= N - 2) : (kk + 1 < kB);
-            const int32_t d = lane == 0 ? -(int32_t)NV - 1 : lane == 1 ? -(int32_t)NV : lane == 2 ? -1
-                            : lane == 3 ? 1 : (int32_t)NV;
-            if (ok) m.noff = __ldg(a.offP + (int32_t)r + d);
-        }
-        // neighbour rows' plane words (garbage for rows without points: never used, see k_count3)
-        const int32_t nrow[5] = {(int32_t)r - (int32_t)NV - 1, (int32_t)r - (int32_t)NV, (int32_t)r - 1, (int32_t)r + 1,
-                                 (int32_t)r + (int32_t)NV};
-        const bool okq[5] = {own && jj >= 1 && kk >= kA + 1, own && kk >= kA + 1, own && jj >= 1, own && jj + 1 <= N - 2,
-                             own && kk + 1 < kB};
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const bool ld = okq[q] && wok;
-            m.nm[q] = ld ? __ldg(a.pmask + (size_t)nrow[q] * W32 + lane) : 0u;
-            m.np[q] = ld ? (uint32_t)__ldg(a.ppre + (size_t)nrow[q] * W32 + lane) : 0u;
-        }
-    };
-
-    RowMeta nx;
-    fetch(rr, j, k, nx);
-    for (; rr < R; rr += warps) {
-        const RowMeta cur = nx;
-        const uint32_t jj = j, kk = k;
-        j += dj; k += dk;
-        if (j >= NV) { j -= NV; ++k; }
-        fetch(rr + warps, j, k, nx);        // next row: in flight while this one is emitted
-        if (cur.cnt == 0) continue;
-        const bool own = (kk >= own0) && (kk < own1);
-        uint32_t noff[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) noff[q] = __shfl_sync(kFull, cur.noff, q);
-        {   // the row's points, listed by running index
-            uint32_t pos = cur.op, m = cur.om;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                slist[warp][pos++] = (uint16_t)(lane * 32 + b);
-            }
-        }
-        __syncwarp();
-        uint32_t run_q = 0, run_s = 0;
-        const size_t rowA = ((size_t)(kk - (uint32_t)a.z_lo) * N + jj) * M;
-        const size_t rowB = rowA + M, rowC = rowA + (size_t)N * M, rowD = rowC + M;
-        for (uint32_t base = 0; base < cur.cnt; base += 32) {
-            const uint32_t t = base + lane;
-            const bool act = t < cur.cnt;
-            const uint32_t i = act ? slist[warp][t] : 0u;    // voxel x
-            const uint32_t wi = cur.offP + t;                // window index
-            const uint32_t g = gid_base + wi;                // global id
-            const uint32_t wl = i >> 5, below = (1u << (i & 31)) - 1u;
-            uint32_t gn[5];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                const uint32_t mw = __shfl_sync(kFull, cur.nm[q], wl), pw = __shfl_sync(kFull, cur.np[q], wl);
-                gn[q] = gid_base + noff[q] + pw + __popc(mw & below);
-            }
-            uint32_t fm = 0, qb = 0, cA = 0, cA1 = 0, cB = 0, cC = 0;
-            if (act && own) {
-                const uint32_t A = code_at<T, ANZ>(lab + rowA + i, ls), A1 = code_at<T, ANZ>(lab + rowA + i + 1, ls);
-                const uint32_t B = code_at<T, ANZ>(lab + rowB + i, ls), B1 = code_at<T, ANZ>(lab + rowB + i + 1, ls);
-                const uint32_t C = code_at<T, ANZ>(lab + rowC + i, ls), C1 = code_at<T, ANZ>(lab + rowC + i + 1, ls);
-                const uint32_t D = code_at<T, ANZ>(lab + rowD + i, ls), D1 = code_at<T, ANZ>(lab + rowD + i + 1, ls);
-                const bool XA = A != A1, XB = B != B1, XC = C != C1, XD = D != D1;
-                const bool YAB = A != B, YA1 = A1 != B1, YCD = C != D, YC1 = C1 != D1;
-                const bool ZAC = A != C, ZA1 = A1 != C1, ZBD = B != D, ZB1 = B1 != D1;
-                fm |= ((XA | XB | YAB | YA1) && kk >= 1) ? 1u : 0u;          // -z
-                fm |= ((XA | XC | ZAC | ZA1) && jj >= 1) ? 2u : 0u;          // -y
-                fm |= ((YAB | YCD | ZAC | ZBD) && i >= 1) ? 4u : 0u;         // -x
-                fm |= ((YA1 | YC1 | ZA1 | ZB1) && i + 3 <= M) ? 8u : 0u;     // +x
-                fm |= ((XB | XD | ZBD | ZB1) && jj + 3 <= N) ? 16u : 0u;     // +y
-                fm |= ((XC | XD | YCD | YC1) && kk + 3 <= (uint32_t)a.O) ? 32u : 0u;   // +z
-                qb |= (XA && jj >= 1 && kk >= 1) ? 1u : 0u;
-                qb |= (YAB && i >= 1 && kk >= 1) ? 2u : 0u;
-                qb |= (ZAC && i >= 1 && jj >= 1) ? 4u : 0u;
-                cA = cls_of_code<T, ANZ>(ls, A); cA1 = cls_of_code<T, ANZ>(ls, A1);
-                cB = cls_of_code<T, ANZ>(ls, B); cC = cls_of_code<T, ANZ>(ls, C);
-            }
-            const uint32_t packed = ((uint32_t)__popc(qb) << 16) | (uint32_t)__popc(fm);
-            const uint32_t x = scan3(packed, lane);
-            const uint32_t tot = __shfl_sync(kFull, x, 31);
-            const uint32_t ex = x - packed;
-            if (act) {
-                a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);
-                a.points[3 * (size_t)wi + 1] = anchor_coord(a.org[1], a.sp[1], jj);
-                a.points[3 * (size_t)wi + 2] = anchor_coord(a.org[2], a.sp[2], kk);
-                if (own) {
-                    const uint32_t o = wi - halo_lo;
-                    uint32_t ss = cur.sbase + run_s + (ex & 0xffffu);
-                    a.fmask[o] = (uint8_t)fm;
-                    a.csr_off[o] = a.first_stencil + ss;
-                    if (fm & 1u) a.csr_ids[ss++] = gn[1];      // -z  (j, k-1)
-                    if (fm & 2u) a.csr_ids[ss++] = gn[2];      // -y  (j-1, k)
-                    if (fm & 4u) a.csr_ids[ss++] = g - 1u;     // -x
-                    if (fm & 8u) a.csr_ids[ss++] = g + 1u;     // +x
-                    if (fm & 16u) a.csr_ids[ss++] = gn[3];     // +y  (j+1, k)
-                    if (fm & 32u) a.csr_ids[ss++] = gn[4];     // +z  (j, k+1)
-                    uint32_t qs = cur.qbase + run_q + (ex >> 16);
-                    if (qb & 1u) {   // x-quad [(j-1,k-1), (j,k-1), (j,k), (j-1,k)]
-                        *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[0], gn[1], g, gn[2]);
-                        *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cA1);
-                        ++qs;
-                    }
-                    if (qb & 2u) {   // y-quad [(i-1,k-1), (i-1,k), (i,k), (i,k-1)] of row j
-                        *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[1] - 1u, g - 1u, g, gn[1]);
-                        *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cB);
-                        ++qs;
-                    }
-                    if (qb & 4u) {   // z-quad [(i-1,j-1), (i,j-1), (i,j), (i-1,j)] of layer k
-                        *reinterpret_cast<uint4 *>(a.quads + 4 * (size_t)qs) = make_uint4(gn[2] - 1u, gn[2], g, g - 1u);
-                        *reinterpret_cast<uint2 *>(a.pairs + 2 * (size_t)qs) = make_uint2(cA, cC);
-                        ++qs;
-                    }
-                }
-            }
-            run_q += tot >> 16;
-            run_s += tot & 0xffffu;
-        }
-        __syncwarp();
-    }
-}
-
 // Pass 4, band-staged (rows of <= 32 plane words).  A CTA emits BANDS of
 // kBand consecutive voxel rows (k-major order, reading Q4).  For each band the
 // point-plane words, per-word prefixes and offsets of every row an id lookup

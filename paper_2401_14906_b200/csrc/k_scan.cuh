@@ -17,7 +17,10 @@
 namespace psn {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 4;
+#ifndef PSN_SCAN_ITEMS
+#define PSN_SCAN_ITEMS 4
+#endif
+constexpr int kScanItems = PSN_SCAN_ITEMS;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 struct TileStatus {           // 64 bytes per tile
@@ -37,12 +40,31 @@ struct ScanHeader {           // device-side header of the extraction workspace
 
 struct ScanArgs {
     const uint32_t *cntP, *cntQ, *cntS;
+    const uint32_t *cntYZ;        // k_count3: y | z << 16 face counts per row (S completed below); NULL = S complete
     uint32_t *offP, *offQ, *offS;
     int64_t R;
     int64_t own_row0, own_row1;   // rows of own layers: [own_row0, own_row1)
+    int64_t NV, kA, O;            // voxel rows per layer, first counted layer, lattice slices
     TileStatus *tiles;
     ScanHeader *hdr;
 };
+
+// Directed stencil entries of voxel row r.  k_count3 counts each shared face once, in the row
+// that owns its lower side (-x, -y, -z of the voxel): the row's +y / +z faces are the -y faces of row
+// j+1 and the -z faces of layer k+1, added here (own rows only; halo rows count points only).
+// (j, k) of row r are passed in (callers step them incrementally: no 64-bit division per row).
+__device__ __forceinline__ uint32_t row_stencil(const ScanArgs &a, int64_t r, int64_t j, int64_t k) {
+    uint32_t s = a.cntS[r];
+    if (a.cntYZ && r >= a.own_row0 && r < a.own_row1) {
+        if (j + 1 < a.NV) s += a.cntYZ[r + 1] & 0xFFFFu;
+        if (k + 3 <= a.O && r + a.NV < a.R) s += a.cntYZ[r + a.NV] >> 16;
+    }
+    return s;
+}
+__device__ __forceinline__ uint32_t row_stencil(const ScanArgs &a, int64_t r) {
+    const int64_t q = r / a.NV;
+    return row_stencil(a, r, r - q * a.NV, a.kA + q);
+}
 
 __device__ __forceinline__ void tile_publish(TileStatus *t, const uint64_t (&v)[3], uint32_t f) {
     if (f == 1) { t->agg[0] = v[0]; t->agg[1] = v[1]; t->agg[2] = v[2]; }
@@ -62,13 +84,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(ScanArgs a) {
 
     uint32_t v[3][kScanItems];
     uint64_t loc[3] = {0, 0, 0};
+    int64_t jr = 0, kr = 0;   // (j, k) of row `base`, stepped per item
+    if (a.cntYZ) { const int64_t q = base / a.NV; jr = base - q * a.NV; kr = a.kA + q; }
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
         const int64_t r = base + it;
         const bool ok = r < a.R;
         v[0][it] = ok ? a.cntP[r] : 0u;
         v[1][it] = ok ? a.cntQ[r] : 0u;
-        v[2][it] = ok ? a.cntS[r] : 0u;
+        v[2][it] = ok ? row_stencil(a, r, jr, kr) : 0u;
+        if (++jr == a.NV) { jr = 0; ++kr; }
 #pragma unroll
         for (int c = 0; c < 3; ++c) loc[c] += v[c][it];
     }

@@ -37,6 +37,7 @@ struct psn_ctx {
     std::vector<uint32_t> label_host;     // bitset or sorted list kept alive for async copies
     // workspaces holding a valid COUNT result, with the volume signature they were counted for
     std::map<const void *, std::array<int64_t, 6>> counted;
+    std::map<const void *, bool> yz_split;   // the COUNT on this workspace was k_count3 (S completed by the scan)
     int smooth_mode = PSN_SMOOTH_PER_ITERATION;   // psn_ctx_set_smoothing (measured faster)
     int32_t smooth_group = 0;                 // iterations per wavefront launch (0 = automatic)
     int32_t smooth_tile = 0;                  // points per wavefront tile (0 = automatic)
@@ -75,7 +76,7 @@ size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 
 struct Layout {
     int64_t M, N, O, kA, kB, R, W32, nTiles;
-    size_t hdr, tiles, cntP, cntQ, cntS, offP, offQ, offS, trim, pmask, ppre, labels, total;
+    size_t hdr, tiles, cntP, cntQ, cntS, cntYZ, offP, offQ, offS, trim, pmask, ppre, labels, total;
 };
 
 constexpr int64_t kMaxList = 65536;   // u32 label-subset capacity in the workspace
@@ -107,6 +108,7 @@ psn_status layout(psn_ctx *ctx, const psn_volume *v, Layout *L) {
     L->cntP = off; off += align_up(4 * (size_t)L->R);
     L->cntQ = off; off += align_up(4 * (size_t)L->R);
     L->cntS = off; off += align_up(4 * (size_t)L->R);
+    L->cntYZ = off; off += align_up(4 * (size_t)L->R);
     L->offP = off; off += align_up(4 * (size_t)L->R);
     L->offQ = off; off += align_up(4 * (size_t)L->R);
     L->offS = off; off += align_up(4 * (size_t)L->R);
@@ -225,9 +227,6 @@ void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cuda
     if (fast && ea.W32 <= 32 && emit_mode == 0) {   // band-staged: shared-memory id lookups
         if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
         else k_emit_band<T, false><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
-    } else if (fast && ea.W32 <= 32 && emit_mode == 1) {   // rows of <= 32 plane words: lane = word, metadata pipelined
-        if (anz) k_emit_row<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
-        else k_emit_row<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
     } else if (fast) {   // rows fit one k_count x-tile: per-word point prefixes are row prefixes
         if (anz) k_emit_fast<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
         else k_emit_fast<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
@@ -358,6 +357,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         ca.labels = slab0; ca.M = L.M; ca.N = L.N; ca.O = L.O; ca.z_lo = vol->z_lo;
         ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W32 = L.W32;
         ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
+        ca.cntYZ = at<uint32_t>(ws, L.cntYZ);
         ca.trim = at<int2>(ws, L.trim); ca.pmask = at<uint32_t>(ws, L.pmask); ca.ppre = at<uint16_t>(ws, L.ppre);
         ca.ls = ls;
         ca.tma = ((L.M * eb) % 16 == 0) && ((reinterpret_cast<uintptr_t>(slab0) & 15u) == 0);
@@ -427,6 +427,8 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         pass_mark(ctx, 1, st);
         ScanArgs sa;
         sa.cntP = ca.cntP; sa.cntQ = ca.cntQ; sa.cntS = ca.cntS;
+        sa.cntYZ = use3 ? ca.cntYZ : nullptr;   // k_count3 counts shared faces once (row_stencil)
+        sa.NV = L.N - 1; sa.kA = L.kA; sa.O = L.O;
         sa.offP = at<uint32_t>(ws, L.offP); sa.offQ = at<uint32_t>(ws, L.offQ); sa.offS = at<uint32_t>(ws, L.offS);
         sa.R = L.R;
         sa.own_row0 = (L.N - 1) * (vol->own_k0 - L.kA);
@@ -437,6 +439,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         pass_mark(ctx, 2, st);
         if ((s = cuda_check(ctx, "count/scan launch")) != PSN_OK) return s;
         ctx->counted[ws] = signature(vol);
+        ctx->yz_split[ws] = use3;
         if (!(phase & PSN_EMIT)) return read_totals(ctx, vol, L, ws, mesh, st, nullptr);
     } else {
         auto it = ctx->counted.find(ws);
@@ -490,13 +493,6 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBandThreads, kBandBufs * sizeof(BandBuf));
         blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + kBand - 1) / kBand, (int64_t)ctx->sms * std::max(occ, 1)));
-    } else if (L.W32 <= 32) {   // k_emit_row: one resident wave of warps, each pipelining its rows
-        int occ = 0;
-        const void *fn = eb == 1 ? (anz ? (const void *)k_emit_row<uint8_t, true> : (const void *)k_emit_row<uint8_t, false>)
-                       : eb == 2 ? (anz ? (const void *)k_emit_row<uint16_t, true> : (const void *)k_emit_row<uint16_t, false>)
-                                 : (anz ? (const void *)k_emit_row<uint32_t, true> : (const void *)k_emit_row<uint32_t, false>);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
-        blocks = std::max<int64_t>(1, std::min<int64_t>((L.R + 7) / 8, (int64_t)ctx->sms * std::max(occ, 1)));
     }
     const bool fast = emode != PSN_EMIT_SCAN &&
                       (L.M - 1) <= (int64_t)(eb == 1 ? count_xt<uint8_t>() : eb == 2 ? count_xt<uint16_t>() : count_xt<uint32_t>());
@@ -509,11 +505,11 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
 }
 
 namespace {
-__global__ void k_rows_out(const uint32_t *cp, const uint32_t *cq, const uint32_t *cs, const int2 *trim, int64_t R,
-                           uint32_t *counts, int2 *trims) {
+__global__ void k_rows_out(ScanArgs sa, const int2 *trim, uint32_t *counts, int2 *trims) {
+    const int64_t R = sa.R;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t p = cp[r];
-        if (counts) { counts[r] = p; counts[R + r] = cq[r]; counts[2 * R + r] = cs[r]; }
+        const uint32_t p = sa.cntP[r];
+        if (counts) { counts[r] = p; counts[R + r] = sa.cntQ[r]; counts[2 * R + r] = row_stencil(sa, r); }
         if (trims) trims[r] = p ? trim[r] : make_int2(0, 0);
     }
 }
@@ -534,10 +530,15 @@ psn_status psn_extract_rows(psn_ctx *ctx, const psn_volume *vol, const void *ws,
     if (!counts && !trims) return PSN_OK;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((L.R + 255) / 256, (int64_t)ctx->sms * 8));
-    k_rows_out<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        at<uint32_t>(const_cast<void *>(ws), L.cntP), at<uint32_t>(const_cast<void *>(ws), L.cntQ),
-        at<uint32_t>(const_cast<void *>(ws), L.cntS), at<int2>(const_cast<void *>(ws), L.trim), L.R, counts,
-        reinterpret_cast<int2 *>(trims));
+    void *w = const_cast<void *>(ws);
+    ScanArgs sa{};
+    sa.cntP = at<uint32_t>(w, L.cntP); sa.cntQ = at<uint32_t>(w, L.cntQ); sa.cntS = at<uint32_t>(w, L.cntS);
+    sa.cntYZ = ctx->yz_split[ws] ? at<uint32_t>(w, L.cntYZ) : nullptr;
+    sa.R = L.R; sa.NV = L.N - 1; sa.kA = L.kA; sa.O = L.O;
+    sa.own_row0 = (L.N - 1) * (vol->own_k0 - L.kA);
+    sa.own_row1 = (L.N - 1) * (vol->own_k1 - L.kA);
+    k_rows_out<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(sa, at<int2>(w, L.trim), counts,
+                                                                             reinterpret_cast<int2 *>(trims));
     return cuda_check(ctx, "rows launch");
 }
 
@@ -784,7 +785,7 @@ psn_status psn_ctx_set_constraint(psn_ctx *ctx, int shape) {
 }
 
 psn_status psn_ctx_set_emission(psn_ctx *ctx, int mode) {
-    if (!ctx || (mode != PSN_EMIT_AUTO && mode != PSN_EMIT_ROW && mode != PSN_EMIT_SCAN)) return PSN_ERR_ARG;
+    if (!ctx || (mode != PSN_EMIT_AUTO && mode != PSN_EMIT_SCAN)) return PSN_ERR_ARG;
     ctx->emit_mode = mode;
     return PSN_OK;
 }

@@ -268,9 +268,12 @@ class SlabPipeline:
         re-cut shards with their halo exchange; returns this rank's share of the
         global smoothed points (ids [cuts[rank], cuts[rank+1]))."""
         total = int(self.table[:, 0].sum())
+        # the ranks' owned id ranges follow from C1's table (no extra all-gather)
+        P = [int(x) for x in self.table[:, 0].tolist()]
+        owned = [(sum(P[:r]), P[r]) for r in range(len(P))]
         self.balanced = BalancedSmoother(self.psn, self.vol, self.mesh, self.first_point, self.first_stencil, total,
                                          self.T, self.lam, self.d, self.group, peer=self.use_peer,
-                                         cache=self._shard_cache)
+                                         cache=self._shard_cache, owned_all=owned)
         return self.balanced.smooth(stream)
 
     def smooth(self, stream=None):
@@ -389,16 +392,17 @@ class BalancedSmoother:
     world coordinates of this rank's own ids [cuts[rank], cuts[rank+1])."""
 
     def __init__(self, psn, vol, mesh, first_point: int, first_stencil: int, total_points: int, iterations: int,
-                 relaxation: float, constraint: float, group=None, peer: bool = False, cache=None):
+                 relaxation: float, constraint: float, group=None, peer: bool = False, cache=None, owned_all=None):
         self.psn, self.vol, self.group = psn, vol, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.T, self.lam, self.d = iterations, relaxation, constraint
         dev = mesh.points.device
         src = balance.source_from_mesh(mesh, first_point, first_stencil)
-        owned = torch.tensor([first_point, mesh.n_points], dtype=torch.int64, device=dev)
-        allo = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(allo, owned, group=group)
-        owned_all = [tuple(int(x) for x in allo[2 * r:2 * r + 2].tolist()) for r in range(self.world)]
+        if owned_all is None:   # (callers with C1's table pass it: no collective here)
+            owned = torch.tensor([first_point, mesh.n_points], dtype=torch.int64, device=dev)
+            allo = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(allo, owned, group=group)
+            owned_all = [tuple(int(x) for x in allo[2 * r:2 * r + 2].tolist()) for r in range(self.world)]
         self.cuts = balance.balanced_cuts(total_points, self.world)
         moves = balance.plan_moves(owned_all, self.cuts)
         self.shard = assemble_batched(self.rank, self.cuts, moves, src, dev, group)
@@ -409,12 +413,13 @@ class BalancedSmoother:
         self.halo = balance.halo_moves(self.cuts, self.windows)
         self.mesh = balance.shard_mesh(psn, self.shard)
         nw = max(self.shard.w1 - self.shard.w0, 1)
-        self.sws = psn.smooth_workspace(self.mesh)
         self.peer = None
         key = (tuple(self.cuts), tuple(self.windows))
-        if cache is not None and key in cache:   # same shard layout as an earlier step: reuse buffers + IPC maps
-            self.buf, self.peer = cache[key]
+        if cache is not None and key in cache:   # same shard layout as an earlier step: reuse buffers, IPC maps,
+            self.buf, self.peer, self.sws, self.out = cache[key]   # workspace and output
         else:
+            self.sws = psn.smooth_workspace(self.mesh)
+            self.out = torch.empty((nw, 3), dtype=torch.float32, device=dev)
             self.buf = [psn.offsets_buffer(nw, dev) for _ in range(2)]   # float4 offsets
             if peer:
                 try:
@@ -423,12 +428,11 @@ class BalancedSmoother:
                 except ValueError:
                     self.peer = None   # a non-adjacent halo move: C2 over NCCL
             if cache is not None:
-                for (_, old_peer) in cache.values():
-                    if old_peer is not None:
-                        old_peer.close()
+                for ent in cache.values():
+                    if ent[1] is not None:
+                        ent[1].close()
                 cache.clear()
-                cache[key] = (self.buf, self.peer)
-        self.out = torch.empty((nw, 3), dtype=torch.float32, device=dev)
+                cache[key] = (self.buf, self.peer, self.sws, self.out)
 
     def smooth(self, stream=None):
         sh = self.shard

@@ -397,7 +397,7 @@ class PSN:
         self._check(self.L.psn_ctx_set_constraint(self.h, int(shape)))
 
     def set_emission(self, mode: int = 0):
-        """0 = automatic (band-staged k_emit_band), 1 = k_emit_row, 2 = general scan-based k_emit."""
+        """0 = automatic (band-staged k_emit_band), 2 = general scan-based k_emit."""
         self._check(self.L.psn_ctx_set_emission(self.h, int(mode)))
 
     def smooth_status(self, mesh: Mesh, ws: torch.Tensor, stream=None):
