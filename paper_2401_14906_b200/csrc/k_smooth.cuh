@@ -229,6 +229,20 @@ __global__ void __launch_bounds__(256) k_smooth_prep8(const uint8_t *fmask, cons
     }
 }
 
+// Streaming accesses of the per-iteration kernel: the packed smoothing cache is read once per iteration
+// and never reused within it, the destination offsets are only read again by the next iteration (long
+// after they left L2 on the large configs) -- keep both out of L1 so it serves the neighbour gathers.
+// (Measured: c4 smoothing 8.01 -> 7.73 ms, c5a 12.26 -> 11.91 ms, c3 unchanged.)
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2 *p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream_f4(float4 *p, float4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w) : "memory");
+}
+
 // Offset-buffer load: read-only path normally; for the peer step, whose halo entries are written by the
 // neighbours over NVLink while the kernel runs (.nc data must stay unchanged for the kernel's lifetime),
 // a coherent L2 load.
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     // PREF: the next grid-stride step's cache entry is loaded one step ahead, so only the
     // neighbour gathers (not cache -> gathers) are on each step's critical path
     uint2 e_next = make_uint2(0u, 0u);
-    if (PACKED && PREF && base0 < n) e_next = __ldg(a.nbr8 + min(base0 + lane, n - 1u));
+    if (PACKED && PREF && base0 < n) e_next = ld_stream_u2(a.nbr8 + min(base0 + lane, n - 1u));
     for (uint32_t base = base0; base < n; base += stride) {
         const uint32_t i = base + lane;
         const bool act = i < n;
@@ -277,9 +291,9 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
             uint2 e;
             if constexpr (PREF) {
                 e = e_next;
-                if (base + stride < n) e_next = __ldg(a.nbr8 + min(base + stride + lane, n - 1u));
+                if (base + stride < n) e_next = ld_stream_u2(a.nbr8 + min(base + stride + lane, n - 1u));
             } else {
-                e = __ldg(a.nbr8 + ii);
+                e = ld_stream_u2(a.nbr8 + ii);
             }
             f = act ? nbr8_faces(e) : 0u;
             nb = nbr8_idx(e, w);
@@ -316,7 +330,7 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
             a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
         } else {
             const float4 r4 = make_float4(r.x, r.y, r.z, 0.f);
-            a.dst[w] = r4;
+            st_stream_f4(a.dst + w, r4);
             if constexpr (PEER) {   // boundary layers also go straight into the neighbours' halos
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
