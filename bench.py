@@ -289,6 +289,12 @@ def run_psn(args, rank, world, local_rank):
         pipe = Pipeline(psn, vol, T, lam, d, triangulate=tri, smooth_cache=args.smooth_cache)
         P, Q, S = pipe.counts
         run_extract, run_smooth = pipe.extract, pipe.smooth
+        if not args.no_graph:
+            # warm the library's one-time host setup, then replay the step as two CUDA graphs (one launch
+            # each): the small configs are bound by the per-kernel host launch path otherwise
+            pipe.run()
+            pipe.capture()
+            run_extract, run_smooth = pipe.replay_extract, pipe.replay_smooth
     else:
         from paper_2401_14906_b200.dist import SlabPipeline, partition, slab_slices
         k0, k1 = partition(O - 1, world)[rank]
@@ -326,6 +332,7 @@ def run_psn(args, rank, world, local_rank):
         launches = sum(pipe.launches.values())
 
     K = args.steps
+    graphs = world == 1 and not args.no_graph
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     # per-pass events recorded by the library between its launches (psn_ctx_set_pass_events)
     pev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -344,7 +351,8 @@ def run_psn(args, rank, world, local_rank):
     for s in range(K):
         if flush is not None:   # inputs fit in L2: flush it between timed steps (outside the events)
             flush.zero_()
-        psn.set_pass_events(pev[s])
+        if not graphs:
+            psn.set_pass_events(pev[s])
         ev[s][0].record(stream)
         run_extract()
         ev[s][1].record(stream)
@@ -353,6 +361,14 @@ def run_psn(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clk.mark(False)
     psn.set_pass_events(None)
+    if graphs:   # per-pass times from K direct (non-graph) extractions: the pass events are host calls
+        for s in range(K):
+            if flush is not None:
+                flush.zero_()
+            psn.set_pass_events(pev[s])
+            pipe.extract()
+        torch.cuda.synchronize()
+        psn.set_pass_events(None)
     barrier()
     time.sleep(0.05)
     clk.__exit__(None, None, None)
@@ -459,6 +475,8 @@ def run_psn(args, rank, world, local_rank):
                                        + (", halo: kernel peer pushes (NVLink, CUDA IPC)" if halo_peer
                                           else ", halo: NCCL point-to-point"))
                        if world > 1 else "single GPU",
+                       "launch": "step replayed as 2 CUDA graphs (extraction, smoothing); per_pass from direct calls"
+                       if graphs else "direct library calls",
                        "l2": ("inputs larger than L2 (%.2f GB labels, %.2f GB smoothing state)" % (V * b / 1e9, P * 28 / 1e9))
                        if V * b > l2 else "inputs fit in L2: L2 flushed (2x L2 written) before every timed step"},
             "counts": {"points": P, "quads": Q, "stencil": S},
@@ -488,6 +506,8 @@ def main():
     ap.add_argument("--nccl-halo", action="store_true",
                     help="N > 1: smoothing halo exchange over NCCL point-to-point instead of the kernel's peer pushes")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N = 1: call the library per step instead of replaying the step's CUDA graphs")
     ap.add_argument("--smooth-cache", action="store_true",
                     help="N = 1: the emission writes the packed smoothing cache next to the stencils and psn_smooth "
                          "skips k_smooth_prep8 (measured: c4 step -0.2 %, extraction +3 %; c5a step -1.6 %)")

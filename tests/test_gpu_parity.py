@@ -435,3 +435,35 @@ def test_surface_nets_stream_matches_single_calls():
     pts_h, q_h, pr_h = sns.result(tickets[-1])
     np.testing.assert_array_equal(pts_h.numpy(), expected[-1][0])
     np.testing.assert_array_equal(q_h.numpy().view(np.uint32), expected[-1][1])
+
+
+@pytest.mark.parametrize("name", ["c1", "c5b"])
+def test_pipeline_graph_replay_identical(name):
+    """bench.py replays the steady-state step as two CUDA graphs (Pipeline.capture): the replayed
+    extraction + smoothing (+ triangulation) write exactly what the direct library calls write."""
+    from paper_2401_14906_b200.psn import Pipeline
+    spec = psn_gen.config(name)
+    T, lam, d = psn_gen.SMOOTHING[name]
+    p = gu.psn()
+    labels = psn_gen.generate_device(spec)
+    vol = p.volume(labels, spacing=tuple(spec.spacing))
+    pipe = Pipeline(p, vol, T, lam, d, triangulate=True)
+    pipe.run()
+    torch.cuda.synchronize()
+    m = pipe.mesh
+    P, Q, S = pipe.counts
+    ref = [t.clone() for t in (m.points[:P], m.quads[:Q], m.pairs[:Q], m.stencil_offsets[:P + 1],
+                               m.stencil_ids[:S], m.face_masks[:P], pipe.out[:P], pipe.tris[:2 * Q])]
+    for t in (m.points, m.quads, m.stencil_ids, pipe.out, pipe.tris):
+        t.zero_()
+    pipe.capture()
+    for t in (m.points, m.quads, m.stencil_ids, pipe.out, pipe.tris):
+        t.zero_()
+    pipe.replay_extract()
+    pipe.replay_smooth()
+    torch.cuda.synchronize()
+    assert pipe.check()
+    got = (m.points[:P], m.quads[:Q], m.pairs[:Q], m.stencil_offsets[:P + 1], m.stencil_ids[:S], m.face_masks[:P],
+           pipe.out[:P], pipe.tris[:2 * Q])
+    for a_, b_ in zip(ref, got):
+        assert torch.equal(a_, b_)
