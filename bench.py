@@ -185,8 +185,12 @@ def oracle_sample(cfg: str, n_layers: int, labels_host=None):
     return dt, M * N * n_layers, (k0, k1), labels_host
 
 
+_PINNED = {"core": None}
+
+
 def host_info():
-    """lscpu model, online CPUs, and the core the oracle is pinned to (SURVEY 8(d) oracle timing)."""
+    """lscpu model, online CPUs, and the core the oracle was pinned to (SURVEY 8(d) oracle timing;
+    None if the pinning was refused, e.g. core 0 outside the process's cpuset)."""
     model = None
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -196,7 +200,7 @@ def host_info():
                 break
     except Exception:
         pass
-    return {"cpu_model": model, "nproc": os.cpu_count(), "pinned_core": 0, "threads_used": 1}
+    return {"cpu_model": model, "nproc": os.cpu_count(), "pinned_core": _PINNED["core"], "threads_used": 1}
 
 
 class pinned_core0:
@@ -206,8 +210,10 @@ class pinned_core0:
         try:
             self.old = os.sched_getaffinity(0)
             os.sched_setaffinity(0, {0})
+            _PINNED["core"] = 0
         except Exception:
             self.old = None
+            _PINNED["core"] = None
         return self
 
     def __exit__(self, *exc):
