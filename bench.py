@@ -302,19 +302,34 @@ def run_psn(args, rank, world, local_rank):
             pipe.capture()
             run_extract, run_smooth = pipe.replay_extract, pipe.replay_smooth
     else:
-        from paper_2401_14906_b200.dist import SlabPipeline, partition, slab_slices
-        k0, k1 = partition(O - 1, world)[rank]
-        z_lo, z_hi = slab_slices(O, k0, k1)
-        labels = psn_gen.generate_device(spec, z_lo, z_hi)
-        # C2 fused into the smoothing kernel (peer pushes over NVLink) unless --nccl-halo
-        pipe = SlabPipeline(psn, labels, (M, N, O), sp, (0.0, 0.0, 0.0), (k0, k1), T, lam, d,
-                            peer=not args.nccl_halo)
+        from paper_2401_14906_b200.dist import (SlabPipeline, balanced_layer_cuts, gather_layer_points,
+                                                partition, slab_slices)
+        own = partition(O - 1, world)[rank]
+
+        def make(own_):
+            z_lo, z_hi = slab_slices(O, own_[0], own_[1])
+            lab_ = psn_gen.generate_device(spec, z_lo, z_hi)
+            # C2 fused into the smoothing kernel (peer pushes over NVLink) unless --nccl-halo
+            return lab_, SlabPipeline(psn, lab_, (M, N, O), sp, (0.0, 0.0, 0.0), own_, T, lam, d,
+                                      peer=not args.nccl_halo)
+
+        labels, pipe = make(own)
+        if args.partition == "points":
+            # equal z-slabs leave c4's per-rank point counts at up to 1.5x the mean at 8 ranks and
+            # smoothing is ~85 % of the step: re-cut the LAYERS once so every rank holds ~P/N points
+            # (from the per-layer counts, all-gathered), then extract and smooth on those slabs --
+            # no per-step re-partition (C4) or shard assembly
+            layer_pts = gather_layer_points(psn, pipe.vol, pipe.ws, own)
+            own = balanced_layer_cuts(layer_pts, world)[rank]
+            del pipe, labels
+            torch.cuda.empty_cache()
+            labels, pipe = make(own)
         tab = pipe.table
         P, Q, S = (int(x) for x in tab[:, :3].sum(0))
         run_extract = pipe.extract
-        # smoothing on point-balanced shards (C4): equal slabs leave c4's per-rank point counts at
-        # up to 1.5x the mean at 8 ranks; --no-balance keeps the extraction slabs
-        run_smooth = pipe.smooth if args.no_balance else pipe.smooth_balanced
+        # --partition c4: equal extraction slabs and the point-balanced smoothing re-partition (C4)
+        # every step; --partition equal: smoothing on the extraction slabs
+        run_smooth = pipe.smooth_balanced if args.partition == "c4" else pipe.smooth
     torch.cuda.synchronize()
 
     def barrier():
@@ -331,7 +346,7 @@ def run_psn(args, rank, world, local_rank):
         assert pipe.check(), "steady-state totals differ from the warm-up count"
     halo_peer = False
     if world > 1:
-        ph = pipe.peer_halo if args.no_balance else pipe.balanced.peer
+        ph = pipe.balanced.peer if args.partition == "c4" else pipe.peer_halo
         halo_peer = ph is not None
     launches = 0
     if world == 1:
@@ -388,7 +403,7 @@ def run_psn(args, rank, world, local_rank):
         t_ext, t_sm, t_step, *t_pass = (float(x) for x in tt.tolist())
     clocks = clk.summary()
     if world > 1 and halo_peer:
-        (pipe.peer_halo if args.no_balance else pipe.balanced.peer).check()   # no peer wait timed out
+        (pipe.balanced.peer if args.partition == "c4" else pipe.peer_halo).check()   # no peer wait timed out
 
     peak, peak_src = measured_peaks()
     b_ext, b_sm = algorithmic_bytes(V, b, P, Q, S)
@@ -477,7 +492,9 @@ def run_psn(args, rank, world, local_rank):
             "dtype": {1: "u8", 2: "u16", 4: "u32"}[b] + "/f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[cfg], "dims": [M, N, O], "label_bytes": b, "iterations": T,
                        "relaxation": lam, "constraint_voxels": d, "spacing": list(sp),
-                       "parallelism": (f"z-slab x{world}" + ("" if args.no_balance else ", point-balanced smoothing")
+                       "parallelism": (f"z-slab x{world}" + {"points": " (layers cut to equal point counts)",
+                                                             "c4": ", point-balanced smoothing re-partition (C4)",
+                                                             "equal": " (equal layers)"}[args.partition]
                                        + (", halo: kernel peer pushes (NVLink, CUDA IPC)" if halo_peer
                                           else ", halo: NCCL point-to-point"))
                        if world > 1 else "single GPU",
@@ -508,7 +525,10 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="psn", choices=["psn", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-balance", action="store_true", help="N > 1: smooth on the extraction slabs (no C4 re-cut)")
+    ap.add_argument("--partition", default="points", choices=["points", "c4", "equal"],
+                    help="N > 1: 'points' = voxel-layer slabs cut to equal point counts (from the per-layer counts, "
+                         "once) for extraction and smoothing; 'c4' = equal slabs + the per-step point-balanced "
+                         "smoothing re-partition; 'equal' = equal slabs for both")
     ap.add_argument("--nccl-halo", action="store_true",
                     help="N > 1: smoothing halo exchange over NCCL point-to-point instead of the kernel's peer pushes")
     ap.add_argument("--e2e-steps", type=int, default=8)

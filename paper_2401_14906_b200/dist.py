@@ -43,6 +43,51 @@ def partition(n_layers: int, world: int):
     return [(r * n_layers // world, (r + 1) * n_layers // world) for r in range(world)]
 
 
+def balanced_layer_cuts(layer_points, world: int):
+    """Contiguous voxel-layer ranges with (nearly) equal point counts: rank r owns
+    layers [c_r, c_{r+1}) where c_r is the first layer whose exclusive point prefix reaches
+    r * P / world; every rank owns >= 1 layer.  `layer_points` = points per voxel layer of the
+    whole volume (the same list on every rank, so the cuts agree without a collective)."""
+    n = len(layer_points)
+    if world > n:
+        raise ValueError("more ranks than voxel layers")
+    total = sum(int(x) for x in layer_points)
+    cuts, acc, r = [0], 0, 1
+    for k, x in enumerate(layer_points):
+        # cut before layer k when the points so far reach rank r's share (and layers remain for the rest)
+        while r < world and acc * world >= r * total and k > cuts[-1] and n - k >= world - r:
+            cuts.append(k)
+            r += 1
+        acc += int(x)
+    while r < world:   # degenerate (e.g. no points): equal layers for the remaining ranks
+        cuts.append(max(cuts[-1] + 1, (r * n) // world))
+        r += 1
+    cuts.append(n)
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+def gather_layer_points(psn, vol, ws, own, group=None):
+    """All-gather every rank's per-layer point counts of its own layers (C1 widened, SURVEY 8(e):
+    ~4 B per layer) -> the whole volume's per-layer list (rank order = layer order)."""
+    counts, _ = psn.rows(vol, ws)
+    N = vol.dims[1]
+    kA = own[0] - (1 if own[0] > 0 else 0)
+    P = counts[0].to(torch.int64).view(-1, N - 1).sum(1)[own[0] - kA: own[1] - kA]
+    world = dist.get_world_size(group)
+    n = torch.tensor([P.numel()], dtype=torch.int64, device=P.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    m = int(max(int(x.item()) for x in ns))
+    pad = torch.zeros(m, dtype=torch.int64, device=P.device)
+    pad[:P.numel()] = P
+    outs = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    res = []
+    for o, k in zip(outs, ns):
+        res += o[:int(k.item())].tolist()
+    return res
+
+
 def slab_slices(O: int, k0: int, k1: int):
     """Lattice slices [z_lo, z_hi) a rank owning voxel layers [k0, k1) must hold."""
     return max(k0 - 1, 0), min(k1 + 1, O - 1) + 1

@@ -122,3 +122,25 @@ def test_gloo_balanced_repartition(world):
     for p in procs:
         p.join(timeout=60)
     assert all(v == "ok" for v in res.values()), res
+
+
+def test_balanced_layer_cuts():
+    """dist.balanced_layer_cuts: contiguous layer ranges covering every layer, >= 1 layer per rank, each
+    rank's points within one layer of the ideal share P/world (SURVEY 8(e) point-balanced slabs)."""
+    import random
+    from paper_2401_14906_b200.dist import balanced_layer_cuts
+    rng = random.Random(3)
+    cases = [[0] * 10, [5] * 7, [0, 0, 100, 0, 0, 0, 1, 1], [rng.randint(0, 50) for _ in range(200)],
+             [int(1000 * (1 - abs(k - 500) / 500)) for k in range(1023)]]
+    for pts in cases:
+        for world in (1, 2, 3, 4, 8):
+            if world > len(pts):
+                continue
+            cuts = balanced_layer_cuts(pts, world)
+            assert cuts[0][0] == 0 and cuts[-1][1] == len(pts)
+            assert all(a < b for a, b in cuts) and all(cuts[i][1] == cuts[i + 1][0] for i in range(world - 1))
+            tot = sum(pts)
+            if tot and world > 1:
+                share = tot / world
+                for a, b in cuts:
+                    assert sum(pts[a:b]) <= share + max(pts) + 1e-9

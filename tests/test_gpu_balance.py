@@ -21,10 +21,10 @@ from paper_2401_14906_b200.dist import partition, slab_slices
 pytestmark = pytest.mark.gpu
 
 
-def extract_slabs(p, a, G, spacing):
+def extract_slabs(p, a, G, spacing, parts=None):
     O, N, M = a.shape
     vols, counted, wss = [], [], []
-    for (k0, k1) in partition(O - 1, G):
+    for (k0, k1) in (parts if parts is not None else partition(O - 1, G)):
         z_lo, z_hi = slab_slices(O, k0, k1)
         dev = torch.from_numpy(np.ascontiguousarray(a[z_lo:z_hi])).cuda()
         vol = p.volume(dev, dims=(M, N, O), spacing=spacing, z_lo=z_lo, own=(k0, k1))

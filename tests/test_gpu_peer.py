@@ -138,6 +138,41 @@ def test_peer_balanced_shards_match_single(G):
     np.testing.assert_array_equal(got, s1[:m1.n_points].cpu().numpy())
 
 
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_peer_point_balanced_slabs_match_single(G):
+    """bench.py's default N > 1 partition: voxel-layer slabs cut to equal point counts
+    (dist.balanced_layer_cuts on the per-layer counts from psn_extract_rows), extraction and peer
+    smoothing on those uneven slabs == single-GPU psn_smooth bit for bit."""
+    from paper_2401_14906_b200.dist import balanced_layer_cuts
+    p = gu.psn()
+    host = psn_gen.generate_host(psn_gen.config("c2"))[40:150]
+    O, N, M = host.shape
+    _, vol1, m1, _ = gu.gpu_extract(host)
+    counts, _ = p.rows(vol1, m1.ws)
+    layer_pts = counts[0].to(torch.int64).view(O - 1, N - 1).sum(1).tolist()
+    parts = balanced_layer_cuts(layer_pts, G)
+    assert parts != [(r * (O - 1) // G, (r + 1) * (O - 1) // G) for r in range(G)]   # really uneven
+    T, lam, d = 6, 0.5, 0.5
+    vols, meshes, firsts, total = extract_slabs(p, host, G, (1.0, 1.0, 1.0), parts=parts)
+    pts_per_rank = [m.n_points for m in meshes]
+    assert max(pts_per_rank) <= total / G + max(layer_pts)
+    table = torch.tensor([[m.n_points, m.n_quads, m.n_stencil, m.c.halo_lo_points, m.c.halo_hi_points]
+                          for m in meshes])
+    sws = [p.smooth_workspace(m) for m in meshes]
+    for r in range(G):
+        p.smooth_prepare(vols[r], meshes[r], sws[r])
+    bufs = [[p.offsets_buffer(m.n_window, "cuda") for _ in range(2)] for m in meshes]
+    src = peer_loop(p, vols, meshes, sws, bufs, slab_sends(table), G, T, lam, d)
+    outs = []
+    for r in range(G):
+        out = torch.empty((max(meshes[r].n_window, 1), 3), dtype=torch.float32, device="cuda")
+        p.smooth_finalize(vols[r], meshes[r], src[r], out)
+        outs.append(out)
+    g = concat(meshes, outs)
+    s1 = p.smooth(vol1, m1, T, lam, d)
+    np.testing.assert_array_equal(g["smoothed"], s1[:m1.n_points].cpu().numpy())
+
+
 def test_peer_slab_cut_above_flat_top_face():
     """A slab cut directly above an object's flat top face: rank 1's first own layer holds no
     points while rank 0's last one does, so rank 1 only RECEIVES on its lower side (peer_sides

@@ -97,3 +97,57 @@ def test_peer_halo_two_processes_one_gpu():
     _, vol1, m1, _ = gu.gpu_extract(a)
     ref = p.smooth(vol1, m1, T, 0.5, 0.5)[:m1.n_points].cpu().numpy()
     np.testing.assert_array_equal(got, ref)
+
+
+def _layer_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+    from paper_2401_14906_b200 import PSN
+    from paper_2401_14906_b200.dist import balanced_layer_cuts, gather_layer_points, partition, slab_slices
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        p = PSN(0)
+        a = _volume()
+        O, N, M = a.shape
+        own = partition(O - 1, world)[rank]
+        z_lo, z_hi = slab_slices(O, own[0], own[1])
+        dev = torch.from_numpy(np.ascontiguousarray(a[z_lo:z_hi])).cuda()
+        vol = p.volume(dev, dims=(M, N, O), z_lo=z_lo, own=own)
+        ws = p.workspace(vol)
+        p.count(vol, p.labels(None), ws)
+        pts = gather_layer_points(p, vol, ws, own)
+        if rank == 0:
+            q.put((pts, balanced_layer_cuts(pts, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_layer_points_two_processes():
+    """bench.py's N > 1 partition step across processes: every rank's per-layer point counts (from
+    psn_extract_rows on its slab) all-gathered into the whole volume's list == the single-volume
+    per-layer counts, and the balanced cuts computed from them."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import gpu_util as gu
+    from paper_2401_14906_b200.dist import balanced_layer_cuts
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_layer_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    pts, cuts = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p = gu.psn()
+    a = _volume()
+    O, N, M = a.shape
+    _, vol1, m1, _ = gu.gpu_extract(a)
+    counts, _ = p.rows(vol1, m1.ws)
+    ref = counts[0].to(torch.int64).view(O - 1, N - 1).sum(1).tolist()
+    assert pts == ref
+    assert cuts == balanced_layer_cuts(ref, world)
