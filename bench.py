@@ -344,6 +344,8 @@ def run_psn(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world == 1:
         assert pipe.check(), "steady-state totals differ from the warm-up count"
+    else:
+        pipe.check_totals()
     halo_peer = False
     if world > 1:
         ph = pipe.balanced.peer if args.partition == "c4" else pipe.peer_halo

@@ -55,7 +55,7 @@ typedef enum {
     PSN_TRI_MOST_COPLANAR = 3   /* most co-planar triangle pair (reading Q27) */
 } psn_tri;
 
-enum { PSN_COUNT = 1, PSN_EMIT = 2 };
+enum { PSN_COUNT = 1, PSN_EMIT = 2, PSN_DEVICE = 4 };
 
 typedef struct psn_ctx psn_ctx;   /* opaque HOST object: device id, SM count, last error */
 
@@ -123,6 +123,10 @@ typedef struct {
      * skips building the cache (saves reading the CSR back). */
     uint32_t *smooth_cache;
     int64_t smooth_cache_valid;                  /* out (EMIT) */
+    /* optional (PSN_DEVICE emission): DEVICE int64[3] = first_point, first_quad, first_stencil,
+     * read by the emission kernel instead of first_* -- the cross-rank exclusive scan (C1) can then
+     * stay on the device (e.g. an NCCL all-gather of psn_extract_totals' output + a prefix sum). */
+    const int64_t *first_dev;
 } psn_mesh;
 
 psn_status psn_ctx_create(int device, psn_ctx **out);
@@ -149,10 +153,21 @@ psn_status psn_extract_workspace(const psn_volume *vol, size_t *bytes);
  *       kernel reads the device totals and writes nothing if they exceed the
  *       capacities; the totals are NOT written back to *mesh (call
  *       psn_mesh_totals later to read them and the device status word).
+ *   PSN_DEVICE (with PSN_COUNT and / or PSN_EMIT): no host round trip -- COUNT leaves the
+ *       totals on the device (psn_extract_totals copies them to a device buffer; *mesh is not
+ *       updated), EMIT skips the host capacity check (the kernel checks the device totals against
+ *       the capacities, as in the fused call) and takes mesh->first_dev if set.  The multi-GPU
+ *       steady state: COUNT|DEVICE -> totals -> all-gather + prefix sum on the device -> EMIT|DEVICE.
  * ws must stay untouched between COUNT and EMIT.
  */
 psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *labels,
                        psn_mesh *mesh, unsigned phase, void *ws, size_t ws_bytes, void *stream);
+
+/* Stream-ordered copy of this call's totals from ws into DEVICE int64 out[5] = own points,
+ * quads, stencil entries, halo-lo points, halo-hi points (what PSN_COUNT writes into *mesh on the
+ * host).  For the PSN_DEVICE path; no synchronisation. */
+psn_status psn_extract_totals(psn_ctx *ctx, const psn_volume *vol, const void *ws, size_t ws_bytes, int64_t *out,
+                              void *stream);
 
 /* Synchronising read of the totals and capacity status left in ws by the
  * last psn_extract (for the PSN_COUNT|PSN_EMIT path).  Returns

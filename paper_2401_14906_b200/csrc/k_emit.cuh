@@ -33,6 +33,7 @@ struct EmitArgs {
     uint8_t *fmask;
     int64_t cap_points, cap_quads, cap_stencil;
     uint32_t first_point, first_quad, first_stencil;
+    const int64_t *first_dev;  // if non-NULL: the global first ids (point, quad, stencil) in device memory
     ScanHeader *hdr;
     uint2 *scache;             // if non-NULL (k_emit_band): packed smoothing cache of the own points
 };
@@ -77,6 +78,10 @@ __global__ void __launch_bounds__(256, 3) k_emit(EmitArgs a) {
         __syncthreads();
     }
     // device-side capacity check (steady-state COUNT|EMIT path)
+    if (a.first_dev) {   // device-side C1 (multi-GPU step without a host round trip)
+        a.first_point = (uint32_t)a.first_dev[0]; a.first_quad = (uint32_t)a.first_dev[1];
+        a.first_stencil = (uint32_t)a.first_dev[2];
+    }
     const uint64_t totP = a.hdr->total[0], totQ = a.hdr->total[1], totS = a.hdr->total[2];
     const uint32_t halo_lo = (uint32_t)a.hdr->halo_lo;
     if (totP > (uint64_t)a.cap_points || totQ > (uint64_t)a.cap_quads || totS > (uint64_t)a.cap_stencil) {
@@ -262,6 +267,10 @@ __global__ void __launch_bounds__(256) k_emit_fast(EmitArgs a) {
         for (int t = threadIdx.x; t < (sizeof(T) == 1 ? 8 : 2048); t += blockDim.x) sbits[t] = a.ls.bits[t];
         ls.bits = sbits;
         __syncthreads();
+    }
+    if (a.first_dev) {   // device-side C1 (multi-GPU step without a host round trip)
+        a.first_point = (uint32_t)a.first_dev[0]; a.first_quad = (uint32_t)a.first_dev[1];
+        a.first_stencil = (uint32_t)a.first_dev[2];
     }
     const uint64_t totP = a.hdr->total[0], totQ = a.hdr->total[1], totS = a.hdr->total[2];
     const uint32_t halo_lo = (uint32_t)a.hdr->halo_lo;
@@ -469,6 +478,10 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
         fence_mbar_init();
     }
     __syncthreads();
+    if (a.first_dev) {   // device-side C1 (multi-GPU step without a host round trip)
+        a.first_point = (uint32_t)a.first_dev[0]; a.first_quad = (uint32_t)a.first_dev[1];
+        a.first_stencil = (uint32_t)a.first_dev[2];
+    }
     const uint64_t totP = a.hdr->total[0], totQ = a.hdr->total[1], totS = a.hdr->total[2];
     const uint32_t halo_lo = (uint32_t)a.hdr->halo_lo;
     if (totP > (uint64_t)a.cap_points || totQ > (uint64_t)a.cap_quads || totS > (uint64_t)a.cap_stencil) {

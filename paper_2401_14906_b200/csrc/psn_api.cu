@@ -332,7 +332,9 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     if (s != PSN_OK) return s;
     if (!mesh) return fail(ctx, PSN_ERR_ARG, "mesh is NULL");
     if (!vol->labels) return fail(ctx, PSN_ERR_ARG, "labels pointer is NULL");
-    if (phase == 0 || (phase & ~3u)) return fail(ctx, PSN_ERR_ARG, "phase must be PSN_COUNT, PSN_EMIT or both");
+    if ((phase & 3u) == 0 || (phase & ~7u))
+        return fail(ctx, PSN_ERR_ARG, "phase must be PSN_COUNT, PSN_EMIT or both (optionally | PSN_DEVICE)");
+    const bool on_device = (phase & PSN_DEVICE) != 0;
     if (!ws || ws_bytes < L.total) return fail(ctx, PSN_ERR_ARG, "workspace too small: need %zu bytes", L.total);
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -440,13 +442,13 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         if ((s = cuda_check(ctx, "count/scan launch")) != PSN_OK) return s;
         ctx->counted[ws] = signature(vol);
         ctx->yz_split[ws] = use3;
-        if (!(phase & PSN_EMIT)) return read_totals(ctx, vol, L, ws, mesh, st, nullptr);
+        if (!(phase & PSN_EMIT)) return on_device ? PSN_OK : read_totals(ctx, vol, L, ws, mesh, st, nullptr);
     } else {
         auto it = ctx->counted.find(ws);
         if (it == ctx->counted.end() || it->second != signature(vol))
             return fail(ctx, PSN_ERR_STATE, "PSN_EMIT needs a preceding PSN_COUNT of the same volume on this workspace");
-        if (mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points > mesh->cap_points ||
-            mesh->n_quads > mesh->cap_quads || mesh->n_stencil > mesh->cap_stencil)
+        if (!on_device && (mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points > mesh->cap_points ||
+                           mesh->n_quads > mesh->cap_quads || mesh->n_stencil > mesh->cap_stencil))
             return fail(ctx, PSN_ERR_CAPACITY, "capacity too small: need points %lld quads %lld stencil %lld",
                         (long long)(mesh->halo_lo_points + mesh->n_points + mesh->halo_hi_points),
                         (long long)mesh->n_quads, (long long)mesh->n_stencil);
@@ -469,6 +471,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     ea.cap_points = mesh->cap_points; ea.cap_quads = mesh->cap_quads; ea.cap_stencil = mesh->cap_stencil;
     ea.first_point = (uint32_t)mesh->first_point; ea.first_quad = (uint32_t)mesh->first_quad;
     ea.first_stencil = (uint32_t)mesh->first_stencil;
+    ea.first_dev = mesh->first_dev;
     ea.hdr = at<ScanHeader>(ws, L.hdr);
     ea.scache = nullptr;
     mesh->smooth_cache_valid = 0;
@@ -540,6 +543,29 @@ psn_status psn_extract_rows(psn_ctx *ctx, const psn_volume *vol, const void *ws,
     k_rows_out<<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(sa, at<int2>(w, L.trim), counts,
                                                                              reinterpret_cast<int2 *>(trims));
     return cuda_check(ctx, "rows launch");
+}
+
+namespace {
+__global__ void k_totals_out(const ScanHeader *h, int has_lo, int has_hi, int64_t *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const uint64_t lo = has_lo ? h->halo_lo : 0, before_hi = has_hi ? h->halo_hi : h->total[0];
+        out[0] = (int64_t)(before_hi - lo); out[1] = (int64_t)h->total[1]; out[2] = (int64_t)h->total[2];
+        out[3] = (int64_t)lo; out[4] = (int64_t)(h->total[0] - before_hi);
+    }
+}
+}  // namespace
+
+psn_status psn_extract_totals(psn_ctx *ctx, const psn_volume *vol, const void *ws, size_t ws_bytes, int64_t *out,
+                              void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    Layout L;
+    psn_status s = layout(ctx, vol, &L);
+    if (s != PSN_OK) return s;
+    if (!ws || ws_bytes < L.total || !out) return fail(ctx, PSN_ERR_ARG, "bad workspace or output");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    k_totals_out<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        at<ScanHeader>(const_cast<void *>(ws), L.hdr), L.kA < vol->own_k0 ? 1 : 0, L.kB > vol->own_k1 ? 1 : 0, out);
+    return cuda_check(ctx, "totals launch");
 }
 
 psn_status psn_mesh_totals(psn_ctx *ctx, const psn_volume *vol, psn_mesh *mesh, const void *ws, size_t ws_bytes,

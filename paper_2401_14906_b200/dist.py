@@ -295,18 +295,43 @@ class SlabPipeline:
                              first=(self.first_point, self.first_quad, self.first_stencil))
         self.counted = MeshC.from_buffer_copy(self.mesh.c)
         self.plan = halo_plan(self.table, self.rank)
+        # device-side C1 for the steady-state steps (NCCL): COUNT|DEVICE -> totals -> all-gather ->
+        # prefix sum -> EMIT|DEVICE, no host round trip; the mesh's host fields stay those of this count
+        self.device_c1 = dist.get_backend(group) == "nccl"
+        dev = labels_slab.device
+        self._tot = torch.zeros(5, dtype=torch.int64, device=dev)
+        self._all = torch.zeros(5 * dist.get_world_size(group), dtype=torch.int64, device=dev)
+        self._first = torch.zeros(3, dtype=torch.int64, device=dev)
         nw = self.mesh.n_window
         self.sws = psn.smooth_workspace(self.mesh)
         self.buf = [psn.offsets_buffer(nw, labels_slab.device) for _ in range(2)]   # float4 offsets
         self.out = torch.empty((max(nw, 1), 3), dtype=torch.float32, device=labels_slab.device)
 
     def extract(self, stream=None):
-        """Per-step extraction: COUNT -> C1 (all-gather) -> EMIT (one host sync for the totals)."""
+        """Per-step extraction: COUNT -> C1 (all-gather) -> EMIT.  With NCCL all three stay on the
+        device (steady state: the volume's totals are those of the setup count, checked by
+        check_totals()); otherwise one host sync reads the totals."""
+        if self.device_c1:
+            world = dist.get_world_size(self.group)
+            self.psn.count_device(self.vol, self.labels, self.ws, self._tot, stream)
+            dist.all_gather_into_tensor(self._all, self._tot, group=self.group)
+            torch.sum(self._all.view(world, 5)[:self.rank, :3], 0, out=self._first)
+            self.psn.emit_device(self.vol, self.labels, self.ws, self.mesh, self._first, stream)
+            return
         c = self.psn.count(self.vol, self.labels, self.ws, stream)
         self.first_point, self.first_quad, self.first_stencil, self.table = exchange_totals(
             c.n_points, c.n_quads, c.n_stencil, c.halo_lo_points, c.halo_hi_points, self.buf[0].device, self.group)
         self.psn.emit(self.vol, self.labels, self.ws, c, first=(self.first_point, self.first_quad, self.first_stencil),
                       mesh=self.mesh, stream=stream)
+
+    def check_totals(self):
+        """Synchronising check that the device-side C1 of the last step saw the setup's per-rank totals
+        (the mesh's host fields and the halo plan assume them) and no emission was skipped."""
+        if self.device_c1:
+            got = self._all.view(-1, 5).cpu()
+            if not torch.equal(got, self.table.to(got.dtype)):
+                raise RuntimeError("per-rank totals changed since the setup count: rebuild the SlabPipeline")
+        self.psn.totals(self.vol, self.ws, self.mesh)
 
     def smooth_balanced(self, stream=None):
         """C4 (point-balanced re-partition of this step's mesh) + T Jacobi steps on the

@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PSN_LIB") or os.path.join(_HERE, "libpsn.so")   # PSN_LIB: A/B builds (tools)
 
 PSN_OK, PSN_ERR_ARG, PSN_ERR_LABELS, PSN_ERR_OVERFLOW, PSN_ERR_CAPACITY, PSN_ERR_STATE, PSN_ERR_CUDA = range(7)
-PSN_COUNT, PSN_EMIT = 1, 2
+PSN_COUNT, PSN_EMIT, PSN_DEVICE = 1, 2, 4
 PSN_TRI_FIXED_02, PSN_TRI_SHORTEST, PSN_TRI_MIN_AREA, PSN_TRI_MOST_COPLANAR = 0, 1, 2, 3
 PSN_CONSTRAINT_BOX, PSN_CONSTRAINT_SPHERE = 0, 1
 BACKGROUND = 0xFFFFFFFF
@@ -57,7 +57,8 @@ class MeshC(ctypes.Structure):
                 ("n_points", ctypes.c_int64), ("n_quads", ctypes.c_int64), ("n_stencil", ctypes.c_int64),
                 ("halo_lo_points", ctypes.c_int64), ("halo_hi_points", ctypes.c_int64),
                 ("first_point", ctypes.c_int64), ("first_quad", ctypes.c_int64), ("first_stencil", ctypes.c_int64),
-                ("smooth_cache", ctypes.c_void_p), ("smooth_cache_valid", ctypes.c_int64)]
+                ("smooth_cache", ctypes.c_void_p), ("smooth_cache_valid", ctypes.c_int64),
+                ("first_dev", ctypes.c_void_p)]
 
 
 class IpcHandle(ctypes.Structure):
@@ -98,6 +99,8 @@ def lib():
         L.psn_extract.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(Labels), ctypes.POINTER(MeshC),
                                   ctypes.c_uint, vp, ctypes.c_size_t, vp]
         L.psn_extract.restype = ctypes.c_int
+        L.psn_extract_totals.argtypes = [vp, ctypes.POINTER(Volume), vp, ctypes.c_size_t, vp, vp]
+        L.psn_extract_totals.restype = ctypes.c_int
         L.psn_mesh_totals.argtypes = [vp, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_mesh_totals.restype = ctypes.c_int
         L.psn_extract_rows.argtypes = [vp, ctypes.POINTER(Volume), vp, ctypes.c_size_t, vp, vp,
@@ -152,7 +155,7 @@ def lib():
 
 
 EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
-            "psn_extract_workspace", "psn_extract", "psn_extract_rows", "psn_mesh_totals", "psn_smooth_workspace",
+            "psn_extract_workspace", "psn_extract", "psn_extract_rows", "psn_extract_totals", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
             "psn_ctx_set_smoothing", "psn_ctx_set_pass_events", "psn_smooth_status", "psn_ctx_set_counting",
             "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_smooth_run_peer", "psn_ipc_export",
@@ -276,6 +279,27 @@ class PSN:
                                 _ptr(ws), ws.numel(), _stream(stream))
         self._check(rc)
         return m
+
+    def count_device(self, vol: Volume, labels: Labels, ws: torch.Tensor, totals: torch.Tensor, stream=None):
+        """psn_extract(PSN_COUNT|PSN_DEVICE) + psn_extract_totals: no host round trip; `totals` (device int64[5])
+        receives (P, Q, S, halo_lo, halo_hi) of this call."""
+        m = MeshC()
+        self._check(self.L.psn_extract(self.h, ctypes.byref(vol), ctypes.byref(labels), ctypes.byref(m),
+                                       PSN_COUNT | PSN_DEVICE, _ptr(ws), ws.numel(), _stream(stream)))
+        self._check(self.L.psn_extract_totals(self.h, ctypes.byref(vol), _ptr(ws), ws.numel(), _ptr(totals),
+                                              _stream(stream)))
+
+    def emit_device(self, vol: Volume, labels: Labels, ws: torch.Tensor, mesh: "Mesh", first_dev: torch.Tensor,
+                    stream=None):
+        """psn_extract(PSN_EMIT|PSN_DEVICE) into `mesh` (its capacities and host fields from an earlier
+        count of the same volume) with the global first ids from device int64[3] `first_dev`."""
+        c = MeshC.from_buffer_copy(mesh.c)
+        self._fill(mesh, c, (c.first_point, c.first_quad, c.first_stencil))
+        mesh.c.first_dev = first_dev.data_ptr()
+        rc = self.L.psn_extract(self.h, ctypes.byref(vol), ctypes.byref(labels), ctypes.byref(mesh.c),
+                                PSN_EMIT | PSN_DEVICE, _ptr(ws), ws.numel(), _stream(stream))
+        mesh.c.first_dev = None
+        self._check(rc)
 
     def alloc_mesh(self, n_window, n_points, n_quads, n_stencil, smooth_cache: bool = False) -> Mesh:
         """Exactly sized output arrays; smooth_cache=True adds the packed smoothing cache the

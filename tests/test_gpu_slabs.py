@@ -110,3 +110,36 @@ def test_slab_emulation_c2_four_slabs():
     gu.assert_mesh_equal({k: g[k] for k in ("points", "quads", "pairs", "csr_off", "csr_ids", "face_mask")}, om)
     ref = oracle.smooth(om, (1, 1, 1), 25, 0.5, 0.5)
     assert np.abs(g["smoothed"].astype(np.float64) - ref).max() <= 1e-4
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_device_c1_matches_host_path(G):
+    """The multi-GPU steady state without host round trips: PSN_COUNT|PSN_DEVICE ->
+    psn_extract_totals -> (all-gather, here a concatenation) + prefix sum on the device ->
+    PSN_EMIT|PSN_DEVICE with mesh.first_dev writes exactly what the host-synchronised path writes."""
+    from test_gpu_balance import extract_slabs
+    p = gu.psn()
+    rng = np.random.default_rng(7 + G)
+    a = np.zeros((19, 17, 29), np.uint16)
+    a[1:-1, 1:-1, 1:-1] = rng.integers(0, 4, size=(17, 15, 27))
+    vols, meshes, firsts, total = extract_slabs(p, a, G, (1.0, 1.0, 1.0))
+    ref = [gu.mesh_np(m) for m in meshes]
+    lab = p.labels(None)
+    wss = [p.workspace(v) for v in vols]
+    tots = [torch.zeros(5, dtype=torch.int64, device="cuda") for _ in range(G)]
+    for r in range(G):
+        p.count_device(vols[r], lab, wss[r], tots[r])
+    allt = torch.stack(tots)                        # what the NCCL all-gather would deliver
+    for r in range(G):
+        m = meshes[r]
+        for t in (m.points, m.quads, m.pairs, m.stencil_offsets, m.stencil_ids, m.face_masks):
+            t.zero_()
+        first = allt[:r, :3].sum(0)
+        p.emit_device(vols[r], lab, wss[r], m, first)
+    torch.cuda.synchronize()
+    for r in range(G):
+        got = gu.mesh_np(meshes[r])
+        for k in ref[r]:
+            np.testing.assert_array_equal(got[k], ref[r][k])
+        assert tuple(int(x) for x in tots[r].tolist()) == (meshes[r].n_points, meshes[r].n_quads, meshes[r].n_stencil,
+                                                            meshes[r].c.halo_lo_points, meshes[r].c.halo_hi_points)
