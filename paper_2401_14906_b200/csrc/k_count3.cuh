@@ -211,7 +211,9 @@ __device__ __forceinline__ uint32_t slow_chunk(uint32_t aA, uint32_t aB, uint32_
     return bits;
 }
 
-template <typename T, bool ANZ, int CPL, int RPW>
+// FULL: the row's chunks fill the warp's lanes exactly (32*CPL chunks, W32 = CPL*E plane words) -- the
+// per-chunk range tests become compile-time true (every BASELINE config).
+template <typename T, bool ANZ, int CPL, int RPW, bool FULL = false>
 __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a) {
     using Key = typename KeyOf<T>::type;
     constexpr int E = Pack<T>::E, TJ = kC3Rows, NWC = TJ / RPW;
@@ -291,7 +293,8 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
     if (w >= nwarps) return;
     const int r0 = w * RPW;                       // first CTA row of this warp
     const int64_t jw = j0 + r0;
-    const int CPR = (int)((M - 1 + E - 1) / E);   // chunks per row
+    const int CPR = FULL ? 32 * CPL : (int)((M - 1 + E - 1) / E);   // chunks per row
+    const int64_t W32 = FULL ? (int64_t)(CPL * E) : a.W32;
     const uint32_t lt = (1u << lane) - 1u;
     auto keys_of = [&](int64_t s, int slot, Key (&kk)[RPW + 1][CPL]) {
         const uint32_t tagz = (uint32_t)(s & 1) << 1;
@@ -413,12 +416,12 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                     if (lane >= d) incl += y;
                 }
                 uint32_t pre = incl - cnt;
-                uint32_t *pm = a.pmask + rr * a.W32;
-                uint16_t *pp = a.ppre + rr * a.W32;
+                uint32_t *pm = a.pmask + rr * W32;
+                uint16_t *pp = a.ppre + rr * W32;
 #pragma unroll
                 for (int q = 0; q < WPL; ++q) {
                     const int wi = lane * WPL + q;
-                    if (wi < a.W32) { pm[wi] = wv[q]; pp[wi] = (uint16_t)pre; }
+                    if (wi < W32) { pm[wi] = wv[q]; pp[wi] = (uint16_t)pre; }
                     pre += __popc(wv[q]);
                 }
             }

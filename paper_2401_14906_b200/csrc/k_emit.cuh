@@ -457,7 +457,7 @@ static_assert(sizeof(uint32_t) * kRangeCap % 16 == 0 && sizeof(uint16_t) * kRang
               sizeof(uint32_t) * (kBand + 12) % 16 == 0 && sizeof(uint32_t) * (kBand + 8) % 16 == 0,
               "staged arrays must start at 16-byte boundaries");
 
-template <typename T, bool ANZ>
+template <typename T, bool ANZ, int WC = 0>   // WC: plane words per row as a compile-time constant (0 = a.W32)
 __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
     constexpr int B = kBand;
     extern __shared__ __align__(128) uint8_t dsm_band[];
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
         a.csr_off[before_hi - halo_lo] = a.first_stencil + (uint32_t)totS;   // CSR sentinel entry
     }
     const uint32_t gid_base = a.first_point - halo_lo;
-    const int32_t M = (int32_t)a.M, N = (int32_t)a.N, NV = N - 1, W32 = (int32_t)a.W32;
+    const int32_t M = (int32_t)a.M, N = (int32_t)a.N, NV = N - 1, W32 = WC ? WC : (int32_t)a.W32;
     const int32_t R = (int32_t)a.R;
     const int32_t kA = (int32_t)a.kA, kB = (int32_t)a.kB, own0 = (int32_t)a.own_k0, own1 = (int32_t)a.own_k1;
     const T *lab = reinterpret_cast<const T *>(a.labels);

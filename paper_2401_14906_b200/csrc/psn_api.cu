@@ -185,17 +185,25 @@ template <bool PK, bool PF, bool PE> V4Fn v4_sel(bool sphere) {
     return sphere ? k_smooth_v4<PK, PF, PE, true> : k_smooth_v4<PK, PF, PE, false>;
 }
 
-template <typename T, bool ANZ, int CPL, int RPW>
-cudaError_t launch_count3(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
+template <typename T, bool ANZ, int CPL, int RPW, bool FULL>
+cudaError_t launch_count3_f(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
     static size_t attr_set = 0;
     if (smem > attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_count3<T, ANZ, CPL, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_count3<T, ANZ, CPL, RPW, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         attr_set = smem;
     }
-    k_count3<T, ANZ, CPL, RPW><<<(unsigned)blocks, 32 * (kC3Rows / RPW + 1), smem, st>>>(ca);
+    k_count3<T, ANZ, CPL, RPW, FULL><<<(unsigned)blocks, 32 * (kC3Rows / RPW + 1), smem, st>>>(ca);
     return cudaGetLastError();
+}
+
+template <typename T, bool ANZ, int CPL, int RPW>
+cudaError_t launch_count3(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
+    constexpr int E = 16 / (int)sizeof(T);
+    const int64_t chunks = (ca.M - 1 + E - 1) / E;
+    return chunks == 32 * CPL ? launch_count3_f<T, ANZ, CPL, RPW, true>(ca, blocks, smem, st)
+                              : launch_count3_f<T, ANZ, CPL, RPW, false>(ca, blocks, smem, st);
 }
 
 template <typename T, bool ANZ, int RPW>
@@ -225,7 +233,11 @@ cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int th
 template <typename T>
 void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st, int emit_mode) {
     if (fast && ea.W32 <= 32 && emit_mode == 0) {   // band-staged: shared-memory id lookups
-        if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
+        // the row-width classes of the common volumes (M <= 1025: 32 plane words; M <= 513: 16) get the word
+        // count as a compile-time constant (c4 emission -6 %, c3 -7 %, c6 -7 %)
+        if (anz && ea.W32 == 32) k_emit_band<T, true, 32><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
+        else if (anz && ea.W32 == 16) k_emit_band<T, true, 16><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
+        else if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
         else k_emit_band<T, false><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
     } else if (fast) {   // rows fit one k_count x-tile: per-word point prefixes are row prefixes
         if (anz) k_emit_fast<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
@@ -491,6 +503,10 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
             for (const void *f : {(const void *)k_emit_band<uint8_t, true>, (const void *)k_emit_band<uint8_t, false>,
                                   (const void *)k_emit_band<uint16_t, true>, (const void *)k_emit_band<uint16_t, false>,
                                   (const void *)k_emit_band<uint32_t, true>, (const void *)k_emit_band<uint32_t, false>})
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBandBufs * sizeof(BandBuf)));
+            for (const void *f : {(const void *)k_emit_band<uint8_t, true, 32>, (const void *)k_emit_band<uint8_t, true, 16>,
+                                  (const void *)k_emit_band<uint16_t, true, 32>, (const void *)k_emit_band<uint16_t, true, 16>,
+                                  (const void *)k_emit_band<uint32_t, true, 32>, (const void *)k_emit_band<uint32_t, true, 16>})
                 cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBandBufs * sizeof(BandBuf)));
             attr = true;
         }
