@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(256) k_emit_fast(EmitArgs a) {
 // at a time (one per lane), neighbour ids are two shared-memory loads + a
 // popcount, and only the 8 corner labels of a point are read from global
 // memory.
-constexpr int kBand = 32;
+#ifndef PSN_BAND_ROWS
+#define PSN_BAND_ROWS 32
+#endif
+constexpr int kBand = PSN_BAND_ROWS;
 constexpr int kBandThreads = 256;
 #ifndef PSN_BAND_BUFS
 #define PSN_BAND_BUFS 2
@@ -715,7 +718,9 @@ __global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
             }
             st.i = st.act ? (uint32_t)(wsel * 32 + bitpos) : 0u;
             if (st.own) {
-                const T *pA = lab + ((size_t)(kk - (int32_t)a.z_lo) * N + jj) * M + st.i;   // rows j, j+1 of slices k, k+1
+                // rows j, j+1 of slices k, k+1 (grid-row index in 32 bits: layers * N < 2^32)
+                const uint32_t grow = (uint32_t)(kk - (int32_t)a.z_lo) * (uint32_t)N + (uint32_t)jj;
+                const T *pA = lab + ((size_t)grow * (uint32_t)M + st.i);
                 const T *pB = pA + M, *pC = pA + (size_t)N * M, *pD = pC + M;
                 st.L[0] = code_at<T, ANZ>(pA, ls); st.L[1] = code_at<T, ANZ>(pA + 1, ls);
                 st.L[2] = code_at<T, ANZ>(pB, ls); st.L[3] = code_at<T, ANZ>(pB + 1, ls);
