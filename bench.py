@@ -454,6 +454,7 @@ def run_psn(args, rank, world, local_rank):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(sns.s_h2d)                       # before the first upload
         tickets = [sns.submit(host) for _ in range(ke)]
+        sns.flush()                                # the last volume's compute (submit defers it by one)
         e1.record(sns.s_d2h)                       # after the last readback
         last = sns.result(tickets[-1])             # host outputs of the last volume are in host memory
         e1.synchronize()

@@ -618,7 +618,9 @@ class SurfaceNetsStream:
                        of the smoothed points.
     `depth` slots (device labels, workspaces, mesh, smoothing buffers, pinned
     host outputs) rotate, so volume s+1's upload overlaps volume s's compute and
-    readback (PCIe is full duplex).  result(ticket) waits for that volume's host
+    readback (PCIe is full duplex); a volume's compute is issued by the NEXT
+    submit() (or result() / flush()), after that volume's upload is queued, so
+    the host's wait for a count never leaves the copy engine idle.  result(ticket) waits for that volume's host
     outputs; they stay valid until `depth` further submissions.  Every step of
     the path runs in libpsn.so's kernels; this class only orders copies and
     launches.
@@ -636,7 +638,8 @@ class SurfaceNetsStream:
         self.slots = [dict(labels=torch.empty(self.shape, dtype=dtype, device=self.dev), ws=None, mesh=None,
                            sws=None, out=None, host=None, counts=None, ev_h2d=torch.cuda.Event(),
                            ev_ext=torch.cuda.Event(), ev_comp=torch.cuda.Event(), ev_d2h=torch.cuda.Event(),
-                           used=False) for _ in range(depth)]
+                           used=False, computed=False) for _ in range(depth)]
+        self._pending = None
         self.n = 0
         self.h2d_bytes = 0
         self.d2h_bytes = 0
@@ -657,6 +660,9 @@ class SurfaceNetsStream:
         sl["sws"] = None
 
     def submit(self, labels_host: torch.Tensor) -> int:
+        """Enqueue the upload of one volume, then run the PREVIOUS volume's compute (its PSN_COUNT
+        synchronises the host on the compute stream): the copy engine already holds this upload,
+        so it never idles while the host waits for a count."""
         if tuple(labels_host.shape) != self.shape or labels_host.dtype != self.dtype:
             raise ValueError("labels_host must match the stream's shape and dtype")
         ticket = self.n
@@ -666,11 +672,25 @@ class SurfaceNetsStream:
                 self.s_h2d.wait_event(sl["ev_comp"])         # the slot's previous volume is processed
             sl["labels"].copy_(labels_host, non_blocking=True)
             sl["ev_h2d"].record(self.s_h2d)
+        sl["used"] = True
+        self.h2d_bytes = labels_host.numel() * labels_host.element_size()
+        self.n += 1
+        self.flush()
+        self._pending = ticket
+        return ticket
+
+    def flush(self):
+        """Run the compute of the last submitted volume if it is still pending (result() does this)."""
+        t = getattr(self, "_pending", None)
+        if t is None:
+            return
+        self._pending = None
+        sl = self.slots[t % self.depth]
         vol = self.psn.volume(sl["labels"], spacing=self.spacing, origin=self.origin)
         if sl["ws"] is None:
             sl["ws"] = self.psn.workspace(vol)
         self.s_comp.wait_event(sl["ev_h2d"])
-        if sl["used"]:
+        if sl["computed"]:
             self.s_comp.wait_event(sl["ev_d2h"])               # the slot's previous outputs are read back
         c = self.psn.count(vol, self.labels, sl["ws"], self.s_comp)   # exact totals (one sync, P:86)
         self._ensure(sl, c)
@@ -690,11 +710,8 @@ class SurfaceNetsStream:
             host["points"][:P].copy_(out[:P], non_blocking=True)
             sl["ev_d2h"].record(self.s_d2h)
         sl["counts"] = (P, Q, mesh.n_stencil)
-        sl["used"] = True
-        self.h2d_bytes = labels_host.numel() * labels_host.element_size()
+        sl["computed"] = True
         self.d2h_bytes = P * 12 + Q * 24
-        self.n += 1
-        return ticket
 
     def _sws_bytes(self, mesh) -> int:
         n = ctypes.c_size_t()
@@ -705,6 +722,8 @@ class SurfaceNetsStream:
         """(points f32 [P,3], quads i32 [Q,4], pairs i32 [Q,2]) on the host for `ticket`."""
         if not (self.n - self.depth <= ticket < self.n):
             raise ValueError("ticket no longer (or not yet) available")
+        if ticket == self._pending:
+            self.flush()
         sl = self.slots[ticket % self.depth]
         sl["ev_d2h"].synchronize()
         P, Q, _ = sl["counts"]
