@@ -301,6 +301,12 @@ psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *poin
  * stream-ordered, no synchronisation.  events == NULL stops the recording. */
 psn_status psn_ctx_set_pass_events(psn_ctx *ctx, void *const *events);
 
+/* Smoothing timing (bench.py's roofline): with events != NULL (2 cudaEvent_t of the context's device),
+ * every later per-iteration psn_smooth records events[0] after its cache preparation (before the
+ * first Jacobi launch) and events[1] after the last one: (events[1] - events[0]) / iterations is the
+ * mean k_smooth_v4 launch time.  NULL stops the recording. */
+psn_status psn_ctx_set_smooth_events(psn_ctx *ctx, void *const *events);
+
 /* Number of kernel launches the last call on this ctx enqueued (bench.py's gpu_launches). */
 int64_t psn_launch_count(const psn_ctx *ctx);
 

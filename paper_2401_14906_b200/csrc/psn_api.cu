@@ -46,6 +46,7 @@ struct psn_ctx {
     int constraint = PSN_CONSTRAINT_BOX;      // psn_ctx_set_constraint
     std::map<void *, void *> ipc_bases;       // psn_ipc_open: returned pointer -> mapped base
     cudaEvent_t pass_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // psn_ctx_set_pass_events
+    cudaEvent_t smooth_ev[2] = {nullptr, nullptr};                      // psn_ctx_set_smooth_events
 };
 
 namespace {
@@ -325,8 +326,23 @@ namespace {
 bool smooth_packed(const psn_ctx *, const psn_volume *vol);   // below, with the smoothing entry points
 }
 
+// Record a timing event on st; inside a stream capture as an external event node (the only kind a replayed
+// graph records for cudaEventElapsedTime), outside one as a plain record.
+static void record_event(cudaEvent_t ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+    else cudaEventRecord(ev, st);
+}
+
 static void pass_mark(const psn_ctx *ctx, int i, cudaStream_t st) {
-    if (ctx->pass_ev[i]) cudaEventRecord(ctx->pass_ev[i], st);
+    if (ctx->pass_ev[i]) record_event(ctx->pass_ev[i], st);
+}
+
+psn_status psn_ctx_set_smooth_events(psn_ctx *ctx, void *const *events) {
+    if (!ctx) return PSN_ERR_ARG;
+    for (int i = 0; i < 2; ++i) ctx->smooth_ev[i] = events ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+    return PSN_OK;
 }
 
 psn_status psn_ctx_set_pass_events(psn_ctx *ctx, void *const *events) {
@@ -761,6 +777,7 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         const V4Fn kern = pick_v4(packed, packed && nw < (1ll << 26), false, cons.sphere != 0);
         const int64_t g4 = v4_grid(ctx, kern, nw);
         const float4 *s4 = nullptr;
+        if (ctx->smooth_ev[0]) record_event(ctx->smooth_ev[0], st);
         for (int32_t t = 0; t < iterations; ++t) {
             const bool last = (t == iterations - 1);
             v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
@@ -768,6 +785,7 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
             ++ctx->launches;
             s4 = v.dst;
         }
+        if (ctx->smooth_ev[1]) record_event(ctx->smooth_ev[1], st);
         return cuda_check(ctx, "smooth launch");
     }
     // wavefront (temporally blocked) smoothing: G iterations per persistent launch

@@ -131,6 +131,8 @@ def lib():
         L.psn_ctx_set_counting.restype = ctypes.c_int
         L.psn_smooth_status.argtypes = [vp, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp]
         L.psn_smooth_status.restype = ctypes.c_int
+        L.psn_ctx_set_smooth_events.argtypes = [vp, ctypes.POINTER(vp)]
+        L.psn_ctx_set_smooth_events.restype = ctypes.c_int
         L.psn_ctx_set_pass_events.argtypes = [vp, ctypes.POINTER(vp)]
         L.psn_ctx_set_pass_events.restype = ctypes.c_int
         L.psn_launch_count.argtypes = [vp]
@@ -157,7 +159,7 @@ def lib():
 EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_string",
             "psn_extract_workspace", "psn_extract", "psn_extract_rows", "psn_extract_totals", "psn_mesh_totals", "psn_smooth_workspace",
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
-            "psn_ctx_set_smoothing", "psn_ctx_set_pass_events", "psn_smooth_status", "psn_ctx_set_counting",
+            "psn_ctx_set_smoothing", "psn_ctx_set_pass_events", "psn_ctx_set_smooth_events", "psn_smooth_status", "psn_ctx_set_counting",
             "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_smooth_run_peer", "psn_ipc_export",
             "psn_ipc_open", "psn_ipc_close"]
 
@@ -411,6 +413,20 @@ class PSN:
         arr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in events])
         self._pass_events = (events, arr)
         self._check(self.L.psn_ctx_set_pass_events(self.h, arr))
+
+    def set_smooth_events(self, events=None):
+        """Record 2 torch.cuda.Events around the Jacobi launches of every later psn_smooth (None: stop)."""
+        if events is None:
+            self._check(self.L.psn_ctx_set_smooth_events(self.h, None))
+            self._smooth_events = None
+            return
+        assert len(events) == 2
+        for e in events:
+            if not e.cuda_event:
+                e.record()
+        arr = (ctypes.c_void_p * 2)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+        self._smooth_events = (events, arr)
+        self._check(self.L.psn_ctx_set_smooth_events(self.h, arr))
 
     def set_counting(self, mode: int = 0):
         """0 = automatic (warp-per-row k_count3 when a row fits a warp), 1 = x-tiled k_count."""
