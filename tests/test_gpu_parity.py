@@ -467,3 +467,22 @@ def test_pipeline_graph_replay_identical(name):
            pipe.out[:P], pipe.tris[:2 * Q])
     for a_, b_ in zip(ref, got):
         assert torch.equal(a_, b_)
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16, np.uint32])
+def test_row_width_class_boundaries(dtype):
+    """Row widths at the edges of the compile-time classes: k_count3's FULL rows (exactly 32*CPL
+    16-byte chunks, CPL = 1, 2, 4) and k_emit_band's 16 / 32 plane words, one element either side,
+    plus one-voxel rows (M = 2) and two-row / two-layer volumes -- bit-exact vs the oracle."""
+    rng = np.random.default_rng(int(np.dtype(dtype).itemsize) * 101)
+    E = 16 // np.dtype(dtype).itemsize
+    widths = {2, 3, 33, 34, 512, 513, 514, 1024, 1025, 1026}
+    for cpl in (1, 2, 4):
+        full = 32 * cpl * E
+        widths |= {full - E + 2, full + 1, full + 2}        # M - 1 = smallest / largest FULL, and one past
+    for M in sorted(w for w in widths if w * np.dtype(dtype).itemsize <= 8192 and w >= 2):
+        for (N, O) in ((5, 4), (2, 3), (3, 2)):
+            a = rng.integers(0, 3, size=(O, N, M)).astype(dtype)
+            if dtype == np.uint32:
+                a = a * np.uint32(0x10001)
+            _check_volume(a, T=2)
