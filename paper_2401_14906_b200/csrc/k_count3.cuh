@@ -213,7 +213,9 @@ __device__ __forceinline__ uint32_t slow_chunk(uint32_t aA, uint32_t aB, uint32_
 
 // FULL: the row's chunks fill the warp's lanes exactly (32*CPL chunks, W32 = CPL*E plane words) -- the
 // per-chunk range tests become compile-time true (every BASELINE config).
-template <typename T, bool ANZ, int CPL, int RPW, bool FULL = false>
+// ROW 2 (EXACT): additionally M == 32*CPL*E (rows of exactly one warp width: c3-c6), so the row length
+// and the staged-row stride are compile-time constants too.
+template <typename T, bool ANZ, int CPL, int RPW, bool FULL = false, bool EXACT = false>
 __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a) {
     using Key = typename KeyOf<T>::type;
     constexpr int E = Pack<T>::E, TJ = kC3Rows, NWC = TJ / RPW;
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t M = a.M, N = a.N, NV = N - 1;
+    const int64_t M = EXACT ? (int64_t)(32 * CPL * Pack<T>::E) : a.M, N = a.N, NV = N - 1;
     const int64_t jb = blockIdx.x % a.nJB, zc = blockIdx.x / a.nJB;
     const int64_t j0 = jb * TJ;
     const int64_t kbeg = a.kA + zc * a.KZ;
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
     const int nrows = (int)min((int64_t)TJ, NV - j0);
     const int nwarps = (nrows + RPW - 1) / RPW;   // active consumer warps
     const int64_t nsteps = kend - kbeg;
-    const uint32_t RB = (uint32_t)a.RB, SB = (TJ + 1) * RB;
+    const uint32_t RB = EXACT ? (uint32_t)(32 * CPL * 16 + 32) : (uint32_t)a.RB, SB = (TJ + 1) * RB;   // (= the host's)
     const uint32_t sbase = smem_u32(dsm);
     const uint32_t copy_bytes = (uint32_t)(M * (int64_t)sizeof(T));
 

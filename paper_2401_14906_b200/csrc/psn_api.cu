@@ -186,16 +186,16 @@ template <bool PK, bool PF, bool PE> V4Fn v4_sel(bool sphere) {
     return sphere ? k_smooth_v4<PK, PF, PE, true> : k_smooth_v4<PK, PF, PE, false>;
 }
 
-template <typename T, bool ANZ, int CPL, int RPW, bool FULL>
+template <typename T, bool ANZ, int CPL, int RPW, bool FULL, bool EXACT>
 cudaError_t launch_count3_f(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
     static size_t attr_set = 0;
     if (smem > attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_count3<T, ANZ, CPL, RPW, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_count3<T, ANZ, CPL, RPW, FULL, EXACT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_set = smem;
     }
-    k_count3<T, ANZ, CPL, RPW, FULL><<<(unsigned)blocks, 32 * (kC3Rows / RPW + 1), smem, st>>>(ca);
+    k_count3<T, ANZ, CPL, RPW, FULL, EXACT><<<(unsigned)blocks, 32 * (kC3Rows / RPW + 1), smem, st>>>(ca);
     return cudaGetLastError();
 }
 
@@ -203,8 +203,14 @@ template <typename T, bool ANZ, int CPL, int RPW>
 cudaError_t launch_count3(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
     constexpr int E = 16 / (int)sizeof(T);
     const int64_t chunks = (ca.M - 1 + E - 1) / E;
-    return chunks == 32 * CPL ? launch_count3_f<T, ANZ, CPL, RPW, true>(ca, blocks, smem, st)
-                              : launch_count3_f<T, ANZ, CPL, RPW, false>(ca, blocks, smem, st);
+    // Exact-width rows (M == 32*CPL*E) get the fully constant row layout where it measured faster:
+    // CPL <= 2 (c3 -4.6%, c5a -13%, c6 -5% count time); at CPL 4 (c4) it was +1.7%.
+    if constexpr (CPL <= 2) {
+        if (ca.M == 32 * CPL * E && ca.RB == 32 * CPL * 16 + 32)
+            return launch_count3_f<T, ANZ, CPL, RPW, true, true>(ca, blocks, smem, st);
+    }
+    return chunks == 32 * CPL ? launch_count3_f<T, ANZ, CPL, RPW, true, false>(ca, blocks, smem, st)
+                              : launch_count3_f<T, ANZ, CPL, RPW, false, false>(ca, blocks, smem, st);
 }
 
 template <typename T, bool ANZ, int RPW>
