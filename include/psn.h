@@ -373,6 +373,75 @@ psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_me
                                size_t ws_bytes, float *buf0, float *buf1, int32_t iterations, float relaxation,
                                float constraint_distance, psn_peer *peer, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Sub-volume blocks stitched into the whole-volume mesh.
+ * boundaries are left open "so that ... distributed execution
+ * avoids introducing artificial partitions along adjacent sub-volume
+ * boundaries"; sub-volumes of a larger input, "with special attention
+ * placed on stitching output meshes together at subvolume boundaries".
+ *
+ * The voxels are cut into a grid of blocks along x, y and z (any cuts).  A
+ * block owning voxels [own_lo, own_hi) is extracted as a STANDALONE volume
+ * (psn_extract with origin 0, spacing 1, z_lo 0, all layers own) over its
+ * lattice box [box_lo, box_hi) = own box plus a one-voxel margin on every
+ * interior side (psn_block_box).  Only that box needs to be in device memory
+ * (psn_block_gather copies it from a host or device volume).  Stitching:
+ *   1. every block:  psn_stitch_count  (its segments' point/quad/stencil counts)
+ *   2. once:         psn_stitch_scan   (exclusive offsets of all segments)
+ *   3. every block:  psn_stitch_emit   (owned points/quads/stencils, global ids)
+ * A SEGMENT is the owned voxels of one block in one voxel row:
+ *   s = (j + (N-1) k) * nxseg + xseg   (global voxel row, x-block index),
+ * nseg = (N-1)(O-1) nxseg.  The stitched mesh (ids, order, every array) is
+ * bit-identical to psn_extract over the whole volume with the same origin,
+ * spacing and label set.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int64_t dims[3];              /* GLOBAL lattice points M, N, O */
+    int64_t own_lo[3], own_hi[3]; /* owned voxel box [own_lo, own_hi), non-empty, inside [0, dims-1) */
+    int64_t box_lo[3], box_hi[3]; /* lattice box of the block's standalone volume (psn_block_box) */
+    int64_t xseg, nxseg;          /* x-block index of the block, number of x-blocks */
+} psn_block;
+
+/* Host-only: box_lo = max(own_lo - 1, 0), box_hi = min(own_hi + 2, dims) per axis (the margin voxel on
+ * each interior side needs one more lattice point).  PSN_ERR_ARG for an empty or out-of-range own box. */
+psn_status psn_block_box(psn_block *blk);
+
+/* Stream-ordered copy of lattice box [box_lo, box_hi) of an x-fastest global volume `src` (host --
+ * pinned for an asynchronous copy -- or device memory, dims[3], element size by dtype) into the compact
+ * device buffer dst[box z][box y][box x].  PSN_ERR_ARG for NULL pointers or a box outside dims. */
+psn_status psn_block_gather(psn_ctx *ctx, const void *src, psn_dtype dtype, const psn_block *blk, void *dst,
+                            void *stream);
+
+/* Device scratch of psn_stitch_count / psn_stitch_emit for one block: uint32[4][(bN-1)(bO-1)] tables
+ * (first / last owned-x point and quad of every local voxel row). */
+psn_status psn_stitch_workspace(const psn_block *blk, size_t *bytes);
+
+/* Step 1 for one block.  `local` = the block's standalone mesh (psn_extract of the box volume:
+ * points, quads, pairs, stencil_offsets, stencil_ids, face_masks, n_points, n_quads).  Fills ws's
+ * tables and, if seg != NULL, writes seg[0][s], seg[1][s], seg[2][s] = points, quads, stencil
+ * entries of every segment this block owns (device uint32[3][nseg]; every segment is written by
+ * exactly one block, so the array needs no clearing).  Re-run with seg == NULL to rebuild ws
+ * before psn_stitch_emit if ws was not kept. */
+psn_status psn_stitch_count(psn_ctx *ctx, const psn_block *blk, const psn_mesh *local, void *ws, size_t ws_bytes,
+                            uint32_t *seg, void *stream);
+
+/* Step 2: off[a][s] = exclusive prefix sum of seg[a][s] over s (a = points, quads, stencil entries;
+ * device uint32[3][nseg] each), totals (device int64[3]) = the sums.  scratch: device bytes
+ * >= psn_stitch_scan_workspace(nseg).  If host_totals != NULL the call synchronises the stream,
+ * copies the totals there and returns PSN_ERR_OVERFLOW if one reaches 2^32. */
+size_t psn_stitch_scan_workspace(int64_t nseg);
+psn_status psn_stitch_scan(psn_ctx *ctx, int64_t nseg, const uint32_t *seg, uint32_t *off, int64_t *totals,
+                           void *scratch, size_t scratch_bytes, int64_t *host_totals, void *stream);
+
+/* Step 3 for one block: writes the block's owned points (recomputed from the global voxel index with
+ * vol->origin / vol->spacing), face masks, stencil offsets and ids, quads and pairs into `global`
+ * (capacities >= the totals; first_* and halo fields ignored: whole-volume ids) and the CSR sentinel
+ * stencil_offsets[P] = S.  ws = this block's tables from psn_stitch_count; off / totals from
+ * psn_stitch_scan.  vol: the global volume (dims must equal blk->dims; labels unused). */
+psn_status psn_stitch_emit(psn_ctx *ctx, const psn_block *blk, const psn_volume *vol, const psn_mesh *local,
+                           const void *ws, size_t ws_bytes, const uint32_t *off, const int64_t *totals,
+                           psn_mesh *global, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

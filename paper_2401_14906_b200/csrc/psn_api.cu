@@ -26,6 +26,7 @@
 #include "k_scan.cuh"
 #include "k_smooth.cuh"
 #include "k_smooth_tb.cuh"
+#include "k_stitch.cuh"
 
 using namespace psn;
 
@@ -1045,6 +1046,184 @@ psn_status psn_triangulate(psn_ctx *ctx, const psn_mesh *mesh, const float *poin
         (int)tri);
     ++ctx->launches;
     return cuda_check(ctx, "triangulate launch");
+}
+
+
+// ---------------------------------------------------------------- sub-volume blocks + stitching (NEXT-4)
+namespace {
+psn_status check_block(psn_ctx *ctx, const psn_block *b, bool need_box) {
+    if (!b) return fail(ctx, PSN_ERR_ARG, "block is NULL");
+    for (int a = 0; a < 3; ++a) {
+        if (b->dims[a] < 2 || b->dims[a] > (1ll << 23)) return fail(ctx, PSN_ERR_ARG, "block dims out of range");
+        if (b->own_lo[a] < 0 || b->own_hi[a] > b->dims[a] - 1 || b->own_lo[a] >= b->own_hi[a])
+            return fail(ctx, PSN_ERR_ARG, "own box must be non-empty inside [0, dims-1)");
+        if (need_box && (b->box_lo[a] != std::max<int64_t>(b->own_lo[a] - 1, 0) ||
+                         b->box_hi[a] != std::min<int64_t>(b->own_hi[a] + 2, b->dims[a])))
+            return fail(ctx, PSN_ERR_ARG, "box must be the own box plus the one-voxel margin (psn_block_box)");
+    }
+    if (b->nxseg < 1 || b->xseg < 0 || b->xseg >= b->nxseg) return fail(ctx, PSN_ERR_ARG, "bad x-block index");
+    if ((b->own_lo[0] > 0) != (b->xseg > 0) || (b->own_hi[0] < b->dims[0] - 1) != (b->xseg < b->nxseg - 1))
+        return fail(ctx, PSN_ERR_ARG, "x-block index inconsistent with the own box");
+    return PSN_OK;
+}
+int64_t block_rows(const psn_block *b) {
+    return (b->box_hi[1] - b->box_lo[1] - 1) * (b->box_hi[2] - b->box_lo[2] - 1);
+}
+size_t stitch_ws_bytes(const psn_block *b) { return 4 * align_up(4 * (size_t)block_rows(b)); }
+
+psn_status stitch_args(psn_ctx *ctx, const psn_block *b, const psn_mesh *local, void *ws, size_t ws_bytes,
+                       StitchArgs *a) {
+    psn_status s = check_block(ctx, b, true);
+    if (s != PSN_OK) return s;
+    if (!local || (local->n_points > 0 && (!local->points || !local->stencil_offsets || !local->face_masks ||
+                                           (local->n_stencil > 0 && !local->stencil_ids))) ||
+        (local->n_quads > 0 && (!local->quads || !local->pairs)) || !local->stencil_offsets)
+        return fail(ctx, PSN_ERR_ARG, "local mesh arrays missing");
+    if (local->halo_lo_points || local->halo_hi_points || local->first_point || local->first_stencil)
+        return fail(ctx, PSN_ERR_ARG, "local mesh must be a standalone extraction (no halos, first ids 0)");
+    if (!ws || ws_bytes < stitch_ws_bytes(b)) return fail(ctx, PSN_ERR_ARG, "stitch workspace too small");
+    if ((reinterpret_cast<uintptr_t>(local->quads) & 15u) || (reinterpret_cast<uintptr_t>(local->pairs) & 7u))
+        return fail(ctx, PSN_ERR_ARG, "quads must be 16-byte and pairs 8-byte aligned");
+    *a = StitchArgs{};
+    a->lpts = local->points; a->lquads = local->quads; a->lpairs = local->pairs;
+    a->lcsr = local->stencil_offsets; a->lids = local->stencil_ids; a->lfm = local->face_masks;
+    a->nP = local->n_points; a->nQ = local->n_quads;
+    a->bM = (int32_t)(b->box_hi[0] - b->box_lo[0]); a->bN = (int32_t)(b->box_hi[1] - b->box_lo[1]);
+    a->bO = (int32_t)(b->box_hi[2] - b->box_lo[2]);
+    for (int d = 0; d < 3; ++d) {
+        a->lo[d] = (int32_t)b->box_lo[d]; a->own_lo[d] = (int32_t)b->own_lo[d]; a->own_hi[d] = (int32_t)b->own_hi[d];
+    }
+    a->N = b->dims[1]; a->xseg = (int32_t)b->xseg; a->nxseg = (int32_t)b->nxseg;
+    const size_t tb = align_up(4 * (size_t)block_rows(b));
+    a->pfirst = at<uint32_t>(ws, 0); a->plast = at<uint32_t>(ws, tb);
+    a->qfirst = at<uint32_t>(ws, 2 * tb); a->qlast = at<uint32_t>(ws, 3 * tb);
+    return PSN_OK;
+}
+}  // namespace
+
+psn_status psn_block_box(psn_block *blk) {
+    psn_status s = check_block(nullptr, blk, false);
+    if (s != PSN_OK) return s;
+    for (int a = 0; a < 3; ++a) {
+        blk->box_lo[a] = std::max<int64_t>(blk->own_lo[a] - 1, 0);
+        blk->box_hi[a] = std::min<int64_t>(blk->own_hi[a] + 2, blk->dims[a]);
+    }
+    return PSN_OK;
+}
+
+psn_status psn_block_gather(psn_ctx *ctx, const void *src, psn_dtype dtype, const psn_block *blk, void *dst,
+                            void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    if (!src || !dst || !blk) return fail(ctx, PSN_ERR_ARG, "NULL argument");
+    if (dtype != PSN_U8 && dtype != PSN_U16 && dtype != PSN_U32) return fail(ctx, PSN_ERR_ARG, "bad dtype");
+    for (int a = 0; a < 3; ++a)
+        if (blk->box_lo[a] < 0 || blk->box_hi[a] > blk->dims[a] || blk->box_lo[a] >= blk->box_hi[a])
+            return fail(ctx, PSN_ERR_ARG, "box outside the volume");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    const size_t b = (size_t)dtype;
+    cudaMemcpy3DParms p{};
+    p.srcPtr = make_cudaPitchedPtr(const_cast<void *>(src), (size_t)blk->dims[0] * b, (size_t)blk->dims[0],
+                                   (size_t)blk->dims[1]);
+    p.srcPos = make_cudaPos((size_t)blk->box_lo[0] * b, (size_t)blk->box_lo[1], (size_t)blk->box_lo[2]);
+    const size_t bm = (size_t)(blk->box_hi[0] - blk->box_lo[0]);
+    p.dstPtr = make_cudaPitchedPtr(dst, bm * b, bm, (size_t)(blk->box_hi[1] - blk->box_lo[1]));
+    p.extent = make_cudaExtent(bm * b, (size_t)(blk->box_hi[1] - blk->box_lo[1]),
+                               (size_t)(blk->box_hi[2] - blk->box_lo[2]));
+    p.kind = cudaMemcpyDefault;
+    if (cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return cuda_check(ctx, "cudaMemcpy3DAsync");
+    return PSN_OK;
+}
+
+psn_status psn_stitch_workspace(const psn_block *blk, size_t *bytes) {
+    if (!blk || !bytes) return PSN_ERR_ARG;
+    psn_status s = check_block(nullptr, blk, true);
+    if (s != PSN_OK) return s;
+    *bytes = stitch_ws_bytes(blk);
+    return PSN_OK;
+}
+
+psn_status psn_stitch_count(psn_ctx *ctx, const psn_block *blk, const psn_mesh *local, void *ws, size_t ws_bytes,
+                            uint32_t *seg, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    StitchArgs a;
+    psn_status s = stitch_args(ctx, blk, local, ws, ws_bytes, &a);
+    if (s != PSN_OK) return s;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(ws, 0xFF, stitch_ws_bytes(blk), st) != cudaSuccess) return cuda_check(ctx, "memset");
+    if (a.nP > 0) { k_stitch_mark_points<<<(unsigned)grid_for(ctx, a.nP), 256, 0, st>>>(a); ++ctx->launches; }
+    if (a.nQ > 0) { k_stitch_mark_quads<<<(unsigned)grid_for(ctx, a.nQ), 256, 0, st>>>(a); ++ctx->launches; }
+    if (seg) {
+        const int64_t nseg = (blk->dims[1] - 1) * (blk->dims[2] - 1) * blk->nxseg;
+        a.segP = seg; a.segQ = seg + nseg; a.segS = seg + 2 * nseg;
+        const int64_t rows = (blk->own_hi[1] - blk->own_lo[1]) * (blk->own_hi[2] - blk->own_lo[2]);
+        k_stitch_segments<<<(unsigned)grid_for(ctx, rows), 256, 0, st>>>(a);
+        ++ctx->launches;
+    }
+    return cuda_check(ctx, "stitch count launch");
+}
+
+size_t psn_stitch_scan_workspace(int64_t nseg) {
+    const int64_t nt = std::max<int64_t>(1, (nseg + kSegTile - 1) / kSegTile);
+    return 3 * (size_t)nt * sizeof(unsigned long long);
+}
+
+psn_status psn_stitch_scan(psn_ctx *ctx, int64_t nseg, const uint32_t *seg, uint32_t *off, int64_t *totals,
+                           void *scratch, size_t scratch_bytes, int64_t *host_totals, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    if (nseg < 1 || nseg > (int64_t)1 << 40 || !seg || !off || !totals)
+        return fail(ctx, PSN_ERR_ARG, "bad segment arrays");
+    if (!scratch || scratch_bytes < psn_stitch_scan_workspace(nseg)) return fail(ctx, PSN_ERR_ARG, "scratch too small");
+    const int64_t nt = (nseg + kSegTile - 1) / kSegTile;
+    if (nt > 65535ll * 1024) return fail(ctx, PSN_ERR_ARG, "too many segments");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto *ts = static_cast<unsigned long long *>(scratch);
+    k_seg_tile_sums<<<dim3((unsigned)nt, 3), kSegThreads, 0, st>>>(seg, nseg, ts);
+    k_seg_scan<<<dim3((unsigned)nt, 3), kSegThreads, 0, st>>>(seg, off, nseg, ts, nt, totals);
+    ctx->launches += 2;
+    psn_status s = cuda_check(ctx, "stitch scan launch");
+    if (s != PSN_OK || !host_totals) return s;
+    if (cudaMemcpyAsync(host_totals, totals, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return cuda_check(ctx, "totals read-back");
+    for (int a = 0; a < 3; ++a)
+        if (host_totals[a] >= ((int64_t)1 << 32)) return fail(ctx, PSN_ERR_OVERFLOW, "stitched total reaches 2^32");
+    return PSN_OK;
+}
+
+psn_status psn_stitch_emit(psn_ctx *ctx, const psn_block *blk, const psn_volume *vol, const psn_mesh *local,
+                           const void *ws, size_t ws_bytes, const uint32_t *off, const int64_t *totals,
+                           psn_mesh *global, void *stream) {
+    if (!ctx) return PSN_ERR_ARG;
+    ctx->launches = 0;
+    StitchArgs a;
+    psn_status s = stitch_args(ctx, blk, local, const_cast<void *>(ws), ws_bytes, &a);
+    if (s != PSN_OK) return s;
+    if (!vol || !off || !totals || !global) return fail(ctx, PSN_ERR_ARG, "NULL argument");
+    for (int d = 0; d < 3; ++d)
+        if (vol->dims[d] != blk->dims[d]) return fail(ctx, PSN_ERR_ARG, "volume dims differ from the block's");
+    if (!global->points || !global->stencil_offsets || !global->face_masks || !global->stencil_ids ||
+        !global->quads || !global->pairs)
+        return fail(ctx, PSN_ERR_ARG, "global mesh arrays missing");
+    if ((reinterpret_cast<uintptr_t>(global->quads) & 15u) || (reinterpret_cast<uintptr_t>(global->pairs) & 7u))
+        return fail(ctx, PSN_ERR_ARG, "quads must be 16-byte and pairs 8-byte aligned");
+    const int64_t nseg = (blk->dims[1] - 1) * (blk->dims[2] - 1) * blk->nxseg;
+    a.offP = off; a.offQ = off + nseg; a.offS = off + 2 * nseg;
+    a.points = global->points; a.quads = global->quads; a.pairs = global->pairs;
+    a.csr = global->stencil_offsets; a.ids = global->stencil_ids; a.fm = global->face_masks;
+    a.totals = totals;
+    for (int d = 0; d < 3; ++d) { a.org[d] = vol->origin[d]; a.sp[d] = vol->spacing[d]; }
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_stitch_points<<<(unsigned)grid_for(ctx, std::max<int64_t>(a.nP, 1)), 256, 0, st>>>(a);
+    ++ctx->launches;
+    if (a.nQ > 0) { k_stitch_quads<<<(unsigned)grid_for(ctx, a.nQ), 256, 0, st>>>(a); ++ctx->launches; }
+    return cuda_check(ctx, "stitch emit launch");
 }
 
 }  // extern "C"

@@ -61,6 +61,12 @@ class MeshC(ctypes.Structure):
                 ("first_dev", ctypes.c_void_p)]
 
 
+class Block(ctypes.Structure):
+    _fields_ = [("dims", ctypes.c_int64 * 3), ("own_lo", ctypes.c_int64 * 3), ("own_hi", ctypes.c_int64 * 3),
+                ("box_lo", ctypes.c_int64 * 3), ("box_hi", ctypes.c_int64 * 3), ("xseg", ctypes.c_int64),
+                ("nxseg", ctypes.c_int64)]
+
+
 class IpcHandle(ctypes.Structure):
     _fields_ = [("handle", ctypes.c_ubyte * 64), ("offset", ctypes.c_uint64)]
 
@@ -152,6 +158,23 @@ def lib():
             L.psn_ipc_open.restype = ctypes.c_int
             L.psn_ipc_close.argtypes = [vp, vp]
             L.psn_ipc_close.restype = ctypes.c_int
+        if hasattr(L, "psn_stitch_emit"):   # (absent from older builds loaded via PSN_LIB)
+            BP = ctypes.POINTER(Block)
+            L.psn_block_box.argtypes = [BP]
+            L.psn_block_box.restype = ctypes.c_int
+            L.psn_block_gather.argtypes = [vp, vp, ctypes.c_int, BP, vp, vp]
+            L.psn_block_gather.restype = ctypes.c_int
+            L.psn_stitch_workspace.argtypes = [BP, ctypes.POINTER(ctypes.c_size_t)]
+            L.psn_stitch_workspace.restype = ctypes.c_int
+            L.psn_stitch_count.argtypes = [vp, BP, ctypes.POINTER(MeshC), vp, ctypes.c_size_t, vp, vp]
+            L.psn_stitch_count.restype = ctypes.c_int
+            L.psn_stitch_scan_workspace.argtypes = [i64]
+            L.psn_stitch_scan_workspace.restype = ctypes.c_size_t
+            L.psn_stitch_scan.argtypes = [vp, i64, vp, vp, vp, vp, ctypes.c_size_t, ctypes.POINTER(ctypes.c_int64), vp]
+            L.psn_stitch_scan.restype = ctypes.c_int
+            L.psn_stitch_emit.argtypes = [vp, BP, ctypes.POINTER(Volume), ctypes.POINTER(MeshC), vp, ctypes.c_size_t,
+                                          vp, vp, ctypes.POINTER(MeshC), vp]
+            L.psn_stitch_emit.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -161,7 +184,8 @@ EXPORTED = ["psn_ctx_create", "psn_ctx_destroy", "psn_last_error", "psn_status_s
             "psn_smooth_prepare", "psn_smooth", "psn_smooth_step", "psn_smooth_finalize", "psn_triangulate", "psn_launch_count",
             "psn_ctx_set_smoothing", "psn_ctx_set_pass_events", "psn_ctx_set_smooth_events", "psn_smooth_status", "psn_ctx_set_counting",
             "psn_ctx_set_emission", "psn_ctx_set_constraint", "psn_smooth_step_peer", "psn_smooth_run_peer", "psn_ipc_export",
-            "psn_ipc_open", "psn_ipc_close"]
+            "psn_ipc_open", "psn_ipc_close", "psn_block_box", "psn_block_gather", "psn_stitch_workspace",
+            "psn_stitch_count", "psn_stitch_scan_workspace", "psn_stitch_scan", "psn_stitch_emit"]
 
 
 def _ptr(t):
