@@ -384,7 +384,7 @@ psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_me
  * block owning voxels [own_lo, own_hi) is extracted as a STANDALONE volume
  * (psn_extract with origin 0, spacing 1, z_lo 0, all layers own) over its
  * lattice box [box_lo, box_hi) = own box plus a one-voxel margin on every
- * interior side (psn_block_box).  Only that box needs to be in device memory
+ * interior side (psn_block_box; a larger box is also valid).  Only that box needs to be in device memory
  * (psn_block_gather copies it from a host or device volume).  Stitching:
  *   1. every block:  psn_stitch_count  (its segments' point/quad/stencil counts)
  *   2. once:         psn_stitch_scan   (exclusive offsets of all segments)
@@ -398,13 +398,18 @@ psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_me
 typedef struct {
     int64_t dims[3];              /* GLOBAL lattice points M, N, O */
     int64_t own_lo[3], own_hi[3]; /* owned voxel box [own_lo, own_hi), non-empty, inside [0, dims-1) */
-    int64_t box_lo[3], box_hi[3]; /* lattice box of the block's standalone volume (psn_block_box) */
+    int64_t box_lo[3], box_hi[3]; /* lattice box of the block's standalone volume: contains the own box plus
+                                     the one-voxel margin on interior sides (psn_block_box) */
     int64_t xseg, nxseg;          /* x-block index of the block, number of x-blocks */
 } psn_block;
 
 /* Host-only: box_lo = max(own_lo - 1, 0), box_hi = min(own_hi + 2, dims) per axis (the margin voxel on
- * each interior side needs one more lattice point).  PSN_ERR_ARG for an empty or out-of-range own box. */
-psn_status psn_block_box(psn_block *blk);
+ * each interior side needs one more lattice point).  With elem_bytes (1, 2 or 4; 0 = tight box) the x
+ * range is then widened inside [0, M) to a multiple of 16 bytes when the volume is wide enough, so the
+ * box rows are TMA-staged by k_count3 (voxels beyond the margin are extracted but never stitched: any
+ * box containing the tight one is valid).  PSN_ERR_ARG for an empty or out-of-range own box, or an
+ * x-block index that contradicts it (xseg > 0 iff own_lo[0] > 0, xseg < nxseg-1 iff own_hi[0] < M-1). */
+psn_status psn_block_box(psn_block *blk, int elem_bytes);
 
 /* Stream-ordered copy of lattice box [box_lo, box_hi) of an x-fastest global volume `src` (host --
  * pinned for an asynchronous copy -- or device memory, dims[3], element size by dtype) into the compact

@@ -52,6 +52,8 @@ class BlockedExtractor:
         self.spacing, self.origin = tuple(spacing), tuple(origin)
         self.label_set = label_set
         self.keep_local = keep_local
+        self.timings = None   # set to {} to collect per-phase CUDA-event times of the next run()
+        self._events = []
         self.nxseg = len(self.cuts[0]) - 1
         self.nseg = (self.dims[1] - 1) * (self.dims[2] - 1) * self.nxseg
         self.blocks = []
@@ -66,7 +68,7 @@ class BlockedExtractor:
                     for d in range(3):
                         blk.own_lo[d], blk.own_hi[d] = lo[d], hi[d]
                     blk.xseg, blk.nxseg = a, self.nxseg
-                    psn._check(psn.L.psn_block_box(ctypes.byref(blk)))
+                    psn._check(psn.L.psn_block_box(ctypes.byref(blk), 0))
                     self.blocks.append(blk)
 
     def global_volume(self, dtype) -> Volume:
@@ -79,14 +81,22 @@ class BlockedExtractor:
         v.z_lo, v.z_hi, v.own_k0, v.own_k1 = 0, self.dims[2], 0, self.dims[2] - 1
         return v
 
+    def _mark(self, name):
+        if self.timings is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._events.append((name, ev))
+
     def _local(self, labels: torch.Tensor, blk: Block, stream):
         psn = self.psn
         shape = tuple(int(blk.box_hi[a] - blk.box_lo[a]) for a in (2, 1, 0))
         buf = torch.empty(shape, dtype=labels.dtype, device=f"cuda:{psn.device}")
         psn._check(psn.L.psn_block_gather(psn.h, ctypes.c_void_p(labels.data_ptr()), _DTYPES[labels.dtype],
                                           ctypes.byref(blk), _ptr(buf), _stream(stream)))
+        self._mark("gather")
         vol = psn.volume(buf)                 # standalone: origin 0, spacing 1 (exact voxel centres)
         mesh = psn.extract(vol, self.label_set, stream=stream)
+        self._mark("extract")
         n = ctypes.c_size_t()
         psn._check(psn.L.psn_stitch_workspace(ctypes.byref(blk), ctypes.byref(n)))
         sws = torch.empty(n.value, dtype=torch.uint8, device=buf.device)
@@ -100,6 +110,10 @@ class BlockedExtractor:
                 tuple(labels.shape) != (self.dims[2], self.dims[1], self.dims[0]):
             raise ValueError("labels must be a contiguous (O, N, M) uint8/uint16/uint32 tensor")
         dev = f"cuda:{psn.device}"
+        for blk in self.blocks:   # x rows of whole 16-byte units (TMA staging) where the volume allows
+            psn._check(psn.L.psn_block_box(ctypes.byref(blk), _DTYPES[labels.dtype]))
+        self._events = []
+        self._mark("start")
         seg = torch.empty((3, self.nseg), dtype=torch.int32, device=dev)
         off = torch.empty_like(seg)
         totals = torch.empty(3, dtype=torch.int64, device=dev)
@@ -108,12 +122,14 @@ class BlockedExtractor:
             mesh, sws = self._local(labels, blk, stream)
             psn._check(psn.L.psn_stitch_count(psn.h, ctypes.byref(blk), ctypes.byref(mesh.c), _ptr(sws), sws.numel(),
                                               _ptr(seg), _stream(stream)))
+            self._mark("stitch_count")
             kept.append((mesh, sws) if self.keep_local else None)
         nbytes = psn.L.psn_stitch_scan_workspace(self.nseg)
         scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         host = (ctypes.c_int64 * 3)()
         psn._check(psn.L.psn_stitch_scan(psn.h, self.nseg, _ptr(seg), _ptr(off), _ptr(totals), _ptr(scratch), nbytes,
                                          host, _stream(stream)))
+        self._mark("stitch_scan")
         P, Q, S = int(host[0]), int(host[1]), int(host[2])
         out = psn.alloc_mesh(P, P, Q, S)
         c = MeshC()
@@ -130,5 +146,11 @@ class BlockedExtractor:
             psn._check(psn.L.psn_stitch_emit(psn.h, ctypes.byref(blk), ctypes.byref(gvol), ctypes.byref(mesh.c),
                                              _ptr(sws), sws.numel(), _ptr(off), _ptr(totals), ctypes.byref(out.c),
                                              _stream(stream)))
+            self._mark("stitch_emit")
         out.volume = gvol
+        if self.timings is not None:   # per-phase device time (ms), summed over blocks
+            torch.cuda.synchronize()
+            self.timings.clear()
+            for (_, a), (name, b) in zip(self._events, self._events[1:]):
+                self.timings[name] = self.timings.get(name, 0.0) + a.elapsed_time(b)
         return out

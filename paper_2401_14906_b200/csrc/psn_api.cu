@@ -1057,9 +1057,9 @@ psn_status check_block(psn_ctx *ctx, const psn_block *b, bool need_box) {
         if (b->dims[a] < 2 || b->dims[a] > (1ll << 23)) return fail(ctx, PSN_ERR_ARG, "block dims out of range");
         if (b->own_lo[a] < 0 || b->own_hi[a] > b->dims[a] - 1 || b->own_lo[a] >= b->own_hi[a])
             return fail(ctx, PSN_ERR_ARG, "own box must be non-empty inside [0, dims-1)");
-        if (need_box && (b->box_lo[a] != std::max<int64_t>(b->own_lo[a] - 1, 0) ||
-                         b->box_hi[a] != std::min<int64_t>(b->own_hi[a] + 2, b->dims[a])))
-            return fail(ctx, PSN_ERR_ARG, "box must be the own box plus the one-voxel margin (psn_block_box)");
+        if (need_box && (b->box_lo[a] < 0 || b->box_lo[a] > std::max<int64_t>(b->own_lo[a] - 1, 0) ||
+                         b->box_hi[a] > b->dims[a] || b->box_hi[a] < std::min<int64_t>(b->own_hi[a] + 2, b->dims[a])))
+            return fail(ctx, PSN_ERR_ARG, "box must contain the own box plus the one-voxel margin (psn_block_box)");
     }
     if (b->nxseg < 1 || b->xseg < 0 || b->xseg >= b->nxseg) return fail(ctx, PSN_ERR_ARG, "bad x-block index");
     if ((b->own_lo[0] > 0) != (b->xseg > 0) || (b->own_hi[0] < b->dims[0] - 1) != (b->xseg < b->nxseg - 1))
@@ -1101,12 +1101,23 @@ psn_status stitch_args(psn_ctx *ctx, const psn_block *b, const psn_mesh *local, 
 }
 }  // namespace
 
-psn_status psn_block_box(psn_block *blk) {
+psn_status psn_block_box(psn_block *blk, int elem_bytes) {
     psn_status s = check_block(nullptr, blk, false);
     if (s != PSN_OK) return s;
+    if (elem_bytes != 0 && elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4) return PSN_ERR_ARG;
     for (int a = 0; a < 3; ++a) {
         blk->box_lo[a] = std::max<int64_t>(blk->own_lo[a] - 1, 0);
         blk->box_hi[a] = std::min<int64_t>(blk->own_hi[a] + 2, blk->dims[a]);
+    }
+    if (elem_bytes) {   // widen x (inside the volume) to rows of a multiple of 16 bytes: TMA-staged rows
+        const int64_t q = 16 / elem_bytes;
+        int64_t w = blk->box_hi[0] - blk->box_lo[0];
+        const int64_t want = (w + q - 1) / q * q;
+        if (want <= blk->dims[0]) {
+            const int64_t grow_hi = std::min(want - w, blk->dims[0] - blk->box_hi[0]);
+            blk->box_hi[0] += grow_hi;
+            blk->box_lo[0] -= want - w - grow_hi;
+        }
     }
     return PSN_OK;
 }

@@ -160,7 +160,7 @@ def lib():
             L.psn_ipc_close.restype = ctypes.c_int
         if hasattr(L, "psn_stitch_emit"):   # (absent from older builds loaded via PSN_LIB)
             BP = ctypes.POINTER(Block)
-            L.psn_block_box.argtypes = [BP]
+            L.psn_block_box.argtypes = [BP, ctypes.c_int]
             L.psn_block_box.restype = ctypes.c_int
             L.psn_block_gather.argtypes = [vp, vp, ctypes.c_int, BP, vp, vp]
             L.psn_block_gather.restype = ctypes.c_int

@@ -48,21 +48,33 @@ def test_block_box_margins():
     for a in range(3):
         b.own_lo[a], b.own_hi[a] = own[a]
     b.xseg, b.nxseg = 0, 2
-    assert L.psn_block_box(ctypes.byref(b)) == P.PSN_OK
+    assert L.psn_block_box(ctypes.byref(b), 0) == P.PSN_OK
     # interior sides get one margin voxel (lattice lo-1 .. hi+1), volume sides none
     assert [b.box_lo[a] for a in range(3)] == [0, 4, 2]
     assert [b.box_hi[a] for a in range(3)] == [9, 15, 6]
+    # 16-byte rows: u16 -> x width a multiple of 8 (grown on the right inside M = 20)
+    assert L.psn_block_box(ctypes.byref(b), 2) == P.PSN_OK
+    assert (b.box_lo[0], b.box_hi[0]) == (0, 16)
+    # last x-block: grown to the left
+    b.own_lo[0], b.own_hi[0], b.xseg = 7, 19, 1
+    assert L.psn_block_box(ctypes.byref(b), 2) == P.PSN_OK
+    assert (b.box_lo[0], b.box_hi[0]) == (4, 20)
+    assert L.psn_block_box(ctypes.byref(b), 1) == P.PSN_OK   # 16 u8 elements
+    assert (b.box_lo[0], b.box_hi[0]) == (4, 20)
+    assert L.psn_block_box(ctypes.byref(b), 3) == P.PSN_ERR_ARG
+    b.own_lo[0], b.own_hi[0], b.xseg = 0, 7, 0
+    assert L.psn_block_box(ctypes.byref(b), 0) == P.PSN_OK
     n = ctypes.c_size_t()
     assert L.psn_stitch_workspace(ctypes.byref(b), ctypes.byref(n)) == P.PSN_OK
     assert n.value >= 4 * 4 * (15 - 4 - 1) * (6 - 2 - 1)
     # inconsistent x-block index / empty box / outside the voxels
     b.xseg = 1
-    assert L.psn_block_box(ctypes.byref(b)) == P.PSN_ERR_ARG
+    assert L.psn_block_box(ctypes.byref(b), 0) == P.PSN_ERR_ARG
     b.xseg = 0
     b.own_hi[2] = 3
-    assert L.psn_block_box(ctypes.byref(b)) == P.PSN_ERR_ARG
+    assert L.psn_block_box(ctypes.byref(b), 0) == P.PSN_ERR_ARG
     b.own_hi[2] = 9
-    assert L.psn_block_box(ctypes.byref(b)) == P.PSN_ERR_ARG
+    assert L.psn_block_box(ctypes.byref(b), 0) == P.PSN_ERR_ARG
 
 
 def test_scan_workspace_size():

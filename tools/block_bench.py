@@ -3,9 +3,9 @@ whole-volume extraction on a BASELINE config (CUDA events around each whole run,
 
     python tools/block_bench.py --config c4 --blocks 2,2,2 --reps 3
 
-Prints one JSON line per variant: whole (device labels, psn.extract), blocks in-core (device labels,
-local meshes kept), blocks out-of-core (pinned host labels, one block resident, re-extracted in the
-emit pass).  Each run includes its host synchronisations (the COUNT read-backs, the stitch totals).
+Prints one JSON line per variant: whole (device labels, psn.extract); blocks in-core (device labels,
+local meshes kept); blocks from pinned host labels (one label box resident at a time, local meshes
+kept); the same with only one block resident at all (re-gathered and re-extracted in the emit pass).  Each run includes its host synchronisations (the COUNT read-backs, the stitch totals).
 """
 import argparse
 import json
@@ -59,12 +59,22 @@ def main():
     bx = BlockedExtractor(p, (M, N, O), blocks=blocks, spacing=sp, keep_local=True)
     bx.run(dev)
     rows.append({"variant": "blocks_in_core", "ms": timed(lambda: bx.run(dev), args.reps)})
+    bh = BlockedExtractor(p, (M, N, O), blocks=blocks, spacing=sp, keep_local=True)
+    bh.run(host)
+    rows.append({"variant": "blocks_host_labels", "ms": timed(lambda: bh.run(host), args.reps)})
     bo = BlockedExtractor(p, (M, N, O), blocks=blocks, spacing=sp, keep_local=False)
     bo.run(host)
-    rows.append({"variant": "blocks_out_of_core_host", "ms": timed(lambda: bo.run(host), args.reps)})
+    rows.append({"variant": "blocks_host_labels_one_resident", "ms": timed(lambda: bo.run(host), args.reps)})
+    for b_, name, src in ((bx, "blocks_in_core", dev), (bh, "blocks_host_labels", host),
+                          (bo, "blocks_host_labels_one_resident", host)):
+        b_.timings = {}
+        b_.run(src)
+        rows.append({"variant": name + "_phases", "ms_by_phase": dict(b_.timings)})
     for r in rows:
-        r.update({"config": args.config, "blocks": list(blocks), "voxels_per_s": vox / (r["ms"] * 1e-3),
+        r.update({"config": args.config, "blocks": list(blocks),
                   "label_bytes": int(host.numel() * host.element_size())})
+        if "ms" in r:
+            r["voxels_per_s"] = vox / (r["ms"] * 1e-3)
         print(json.dumps(r))
 
 
