@@ -18,12 +18,15 @@
 //   the global id of a point is offP[s] + its rank in the segment, and the
 //   quads / stencil entries of a segment are one contiguous range too.
 //
-// Local ids of one local voxel row are consecutive in x, and a local row holds
-// at most one margin voxel on each x side, so per local row the first / last
+// Local ids of one local voxel row are consecutive in x, and the x-owned voxels
+// of a row lie between its margin voxels, so per local row the first / last
 // x-owned point (and owned quad -- quads are voxel-major and their 3rd vertex is
-// the owning voxel, reading Q6) bound the segment.  A referenced point outside
-// the block's x range is the last point of the left segment (offP[s] - 1) or
-// the first of the right one (offP[s + 1]).
+// the owning voxel, reading Q6) bound the segment.  Stencils and quads only
+// reference the +-1 neighbours, so a referenced point outside the block's x
+// range is the last point of the left segment (offP[s] - 1) or the first of the
+// right one (offP[s + 1]).  A stencil entry's voxel follows from its face (the
+// entries are in face order -z,-y,-x,+x,+y,+z = ascending id); a quad vertex's
+// from its local point.
 //
 // Local points are voxel centres fl32(idx + 0.5) (origin 0, spacing 1), which
 // recover the local voxel index exactly (idx < 2^23); the stitched points are
@@ -83,35 +86,42 @@ __device__ __forceinline__ int64_t seg_of(const StitchArgs &a, const LVox &v) {
     return g * a.nxseg + a.xseg;
 }
 
-// First / last x-owned point of every local voxel row (one writer per entry: no atomics).
-__global__ void k_stitch_mark_points(StitchArgs a) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.nP; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t l = (uint32_t)t;
-        const LVox v = lvox(a, l);
-        if (!xown(a, v)) continue;
-        const int32_t r = lrow(a, v);
-        bool prev = false, next = false;
-        if (l > 0) { const LVox u = lvox(a, l - 1); prev = lrow(a, u) == r && xown(a, u); }
-        if (t + 1 < a.nP) { const LVox u = lvox(a, l + 1); next = lrow(a, u) == r && xown(a, u); }
-        if (!prev) a.pfirst[r] = l;
-        if (!next) a.plast[r] = l;
+// First / last x-owned point of every local voxel row (one writer per entry: no atomics).  A warp
+// takes 32 consecutive ids; the neighbours' voxels come by shuffle (one coalesced read per point).
+template <bool QUADS>
+__device__ __forceinline__ void mark_rows(const StitchArgs &a, int64_t n, uint32_t *first, uint32_t *last) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane); base < n; base += nwarps * 32) {
+        const int64_t t = base + lane;
+        auto owner = [&](int64_t x) -> uint32_t {
+            return QUADS ? __ldg(a.lquads + 4 * (size_t)x + 2) : (uint32_t)x;
+        };
+        LVox v{0, 0, -1};
+        if (t < n) v = lvox(a, owner(t));
+        const bool xo = t < n && xown(a, v);
+        const int32_t r = t < n ? lrow(a, v) : -1;
+        int32_t rp = __shfl_up_sync(kFull, r, 1), rn = __shfl_down_sync(kFull, r, 1);
+        bool xp = __shfl_up_sync(kFull, xo, 1), xn = __shfl_down_sync(kFull, xo, 1);
+        if (lane == 0) {
+            rp = -1; xp = false;
+            if (t > 0 && t < n) { const LVox u = lvox(a, owner(t - 1)); rp = lrow(a, u); xp = xown(a, u); }
+        }
+        if (lane == 31) {
+            rn = -1; xn = false;
+            if (t + 1 < n) { const LVox u = lvox(a, owner(t + 1)); rn = lrow(a, u); xn = xown(a, u); }
+        }
+        if (xo) {
+            if (!(xp && rp == r)) first[r] = (uint32_t)t;
+            if (!(xn && rn == r)) last[r] = (uint32_t)t;
+        }
     }
 }
 
+__global__ void k_stitch_mark_points(StitchArgs a) { mark_rows<false>(a, a.nP, a.pfirst, a.plast); }
+
 // First / last quad owned by an x-owned voxel of every local voxel row.
-__global__ void k_stitch_mark_quads(StitchArgs a) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.nQ; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = (uint32_t)t;
-        const LVox v = lvox(a, __ldg(a.lquads + 4 * (size_t)q + 2));
-        if (!xown(a, v)) continue;
-        const int32_t r = lrow(a, v);
-        bool prev = false, next = false;
-        if (q > 0) { const LVox u = lvox(a, __ldg(a.lquads + 4 * (size_t)(q - 1) + 2)); prev = lrow(a, u) == r && xown(a, u); }
-        if (t + 1 < a.nQ) { const LVox u = lvox(a, __ldg(a.lquads + 4 * (size_t)(q + 1) + 2)); next = lrow(a, u) == r && xown(a, u); }
-        if (!prev) a.qfirst[r] = q;
-        if (!next) a.qlast[r] = q;
-    }
-}
+__global__ void k_stitch_mark_quads(StitchArgs a) { mark_rows<true>(a, a.nQ, a.qfirst, a.qlast); }
 
 // Counts of the block's segments: one thread per owned voxel row (every owned segment written once).
 __global__ void k_stitch_segments(StitchArgs a) {
@@ -131,15 +141,15 @@ __global__ void k_stitch_segments(StitchArgs a) {
     }
 }
 
-// Global id of local point m (owned by this block or by a neighbour through the margin).
-__device__ __forceinline__ uint32_t remap(const StitchArgs &a, uint32_t m) {
-    const LVox v = lvox(a, m);
+// Global id of local point m at local voxel v (owned by this block or by a neighbour through the margin).
+__device__ __forceinline__ uint32_t remap_at(const StitchArgs &a, uint32_t m, const LVox &v) {
     const int64_t s = seg_of(a, v);
     const int32_t gi = v.i + a.lo[0];
     if (gi < a.own_lo[0]) return __ldg(a.offP + s) - 1u;   // last point of the left segment
     if (gi >= a.own_hi[0]) return __ldg(a.offP + s + 1);   // first point of the right segment
     return __ldg(a.offP + s) + (m - __ldg(a.pfirst + lrow(a, v)));
 }
+__device__ __forceinline__ uint32_t remap(const StitchArgs &a, uint32_t m) { return remap_at(a, m, lvox(a, m)); }
 
 __global__ void k_stitch_points(StitchArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.csr[a.totals[0]] = (uint32_t)a.totals[2];   // CSR sentinel
@@ -157,7 +167,18 @@ __global__ void k_stitch_points(StitchArgs a) {
         const uint32_t c0 = __ldg(a.lcsr + l), c1 = __ldg(a.lcsr + l + 1);
         const uint32_t base = __ldg(a.offS + s) + (c0 - __ldg(a.lcsr + f));
         a.csr[G] = base;
-        for (uint32_t e = c0; e < c1; ++e) a.ids[base + (e - c0)] = remap(a, __ldg(a.lids + e));
+        // stencil entries are in face order -z, -y, -x, +x, +y, +z over the set bits of the face mask
+        // (= ascending id), so each neighbour's voxel is the owner's +- one step: no point gather
+        uint32_t fmk = __ldg(a.lfm + l), e = c0;
+        while (fmk) {
+            const int f = __ffs(fmk) - 1;
+            fmk &= fmk - 1u;
+            LVox u = v;
+            if (f == 0) --u.k; else if (f == 1) --u.j; else if (f == 2) --u.i;
+            else if (f == 3) ++u.i; else if (f == 4) ++u.j; else ++u.k;
+            a.ids[base + (e - c0)] = remap_at(a, __ldg(a.lids + e), u);
+            ++e;
+        }
     }
 }
 
