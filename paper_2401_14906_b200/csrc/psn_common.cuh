@@ -199,15 +199,6 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-#ifdef PSN_MBAR_HINT
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "n"(PSN_MBAR_HINT)
-        : "memory");
-#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -215,7 +206,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
-#endif
 }
 }  // namespace psn
 
