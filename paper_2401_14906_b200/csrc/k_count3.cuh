@@ -262,6 +262,9 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
 
     if (warp == NWC) {
         // ------------------------------------------------------------ producer
+        const uintptr_t lab_al = reinterpret_cast<uintptr_t>(lab);
+        const int wcp = a.tma ? 0 : ((copy_bytes % 8u) == 0u && (lab_al & 7u) == 0u) ? 8
+                                : ((copy_bytes % 4u) == 0u && (lab_al & 3u) == 0u) ? 4 : 0;
         int slot = 0;
         uint32_t ph = 0;   // parity of the slot's refill round
         for (int64_t s = 0; s <= nsteps; ++s) {
@@ -276,6 +279,22 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                     const int64_t j = min(j0 + lane, N - 1);
                     tma_load_1d(dst + lane * RB, lab + (z * N + j) * M, copy_bytes, &full[slot]);
                 }
+            } else if (wcp) {
+                // rows of a multiple of 4 (8) bytes, not of 16: per-lane cp.async word copies, all in
+                // flight at once; the slot's mbarrier completes when every lane's copies have landed
+                for (int g = 0; g <= TJ; ++g) {
+                    const int64_t j = min(j0 + g, N - 1);
+                    const char *src = reinterpret_cast<const char *>(lab + (z * N + j) * M);
+                    const uint32_t d = smem_u32(dst + g * RB);
+                    if (wcp == 8) {
+                        for (uint32_t x = 8u * lane; x < copy_bytes; x += 256u)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d + x), "l"(src + x) : "memory");
+                    } else {
+                        for (uint32_t x = 4u * lane; x < copy_bytes; x += 128u)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + x), "l"(src + x) : "memory");
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
             } else {
                 for (int g = 0; g <= TJ; ++g) {
                     const int64_t j = min(j0 + g, N - 1);
