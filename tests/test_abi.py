@@ -92,3 +92,33 @@ def test_block_cuts():
             assert all(c[t] < c[t + 1] for t in range(len(c) - 1))
             sizes = [c[t + 1] - c[t] for t in range(len(c) - 1)]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_block_grid_covers_voxels_once():
+    """BlockedExtractor's grid (host logic, no GPU): every voxel owned by exactly one block, every box
+    contains its own box plus the one-voxel margin on interior sides, x-block indices consistent."""
+    import numpy as np
+    P, L = _lib()
+    from paper_2401_14906_b200.blocks import BlockedExtractor
+
+    class Stub:
+        pass
+    s = Stub()
+    s.L = L
+
+    def check(rc):
+        assert rc == P.PSN_OK
+    s._check = check
+    dims = (23, 17, 12)
+    bx = BlockedExtractor(s, dims, blocks=(3, 2, 4))
+    own = np.zeros((dims[2] - 1, dims[1] - 1, dims[0] - 1), np.int32)
+    for b in bx.blocks:
+        lo = [b.own_lo[a] for a in range(3)]; hi = [b.own_hi[a] for a in range(3)]
+        own[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] += 1
+        for a in range(3):
+            assert b.box_lo[a] == max(lo[a] - 1, 0) and b.box_hi[a] == min(hi[a] + 2, dims[a])
+        assert (b.xseg > 0) == (lo[0] > 0) and (b.xseg < b.nxseg - 1) == (hi[0] < dims[0] - 1)
+    assert own.min() == 1 and own.max() == 1
+    assert bx.nseg == (dims[1] - 1) * (dims[2] - 1) * 3
+    with pytest.raises(ValueError):
+        BlockedExtractor(s, dims, cuts=[[0, 5, 5, 22], [0, 16], [0, 11]])
