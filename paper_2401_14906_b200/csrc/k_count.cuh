@@ -53,6 +53,8 @@ struct CountArgs {
     int multi_xt;              // several x-tiles per row: accumulate with global atomics
     int tma;                   // rows are 16-byte aligned: stage with cp.async.bulk
     int NS;                    // k_count3 ring slots
+    int64_t stg_off, RB2;      // k_count3 rows of an odd 1/2-byte length: staging area (dynamic smem offset,
+                               // bytes per staged row) for the TMA copy of each row's 16-byte-aligned superset
 };
 
 template <typename T> __host__ __device__ constexpr int count_tj() { return 4; }

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
     constexpr int WPL = (CPL * E + 31) / 32;     // mask words per lane
     constexpr uint32_t MSB = Flags<T>::FL;   // flag bits of the slow path's planes
     extern __shared__ __align__(128) uint8_t dsm[];
-    __shared__ __align__(8) uint64_t full[kC3MaxStages], empty[kC3MaxStages];
+    __shared__ __align__(8) uint64_t full[kC3MaxStages], empty[kC3MaxStages], sbar;
     __shared__ QItem wq[NWC][RPW * 32 * CPL];   // one layer's non-uniform (row, chunk) items
     __shared__ uint32_t wm[TJ][32 * WPL];
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
             mbar_init(&full[s], a.tma ? 1u : 32u);
             mbar_init(&empty[s], (uint32_t)max(nwarps, 1));
         }
+        mbar_init(&sbar, 1u);
         fence_mbar_init();
     }
     __syncthreads();
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                                 : ((copy_bytes % 4u) == 0u && (lab_al & 3u) == 0u) ? 4 : 0;
         int slot = 0;
         uint32_t ph = 0;   // parity of the slot's refill round
+        uint32_t sph = 0;  // parity of the staging barrier
         for (int64_t s = 0; s <= nsteps; ++s) {
             if (s >= NS) mbar_wait(&empty[slot], ph ^ 1u);
             const int64_t z = kbeg + s - a.z_lo;
@@ -295,6 +297,57 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                     }
                 }
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
+            } else if (a.RB2 > 0) {
+                // rows of an odd 1- / 2-byte length (their starts are not even 4-byte aligned): TMA each
+                // row's 16-byte-aligned superset into the staging area, then shift it into place in
+                // shared memory (16 bytes per lane step; the byte shift is warp-uniform per row)
+                uint8_t *stg = dsm + a.stg_off;
+                const char *row_src = nullptr;
+                uint32_t dl = 0, tb = 0, tail = 0;
+                if (lane <= TJ) {
+                    const int64_t j = min(j0 + lane, N - 1);
+                    row_src = reinterpret_cast<const char *>(lab + (z * N + j) * M);
+                    dl = (uint32_t)(reinterpret_cast<uintptr_t>(row_src) & 15u);
+                    tb = (dl + copy_bytes + 15u) & ~15u;
+                    const char *lim = reinterpret_cast<const char *>(lab + (a.kB + 1 - a.z_lo) * N * M);
+                    const int64_t room = lim - (row_src - dl);   // never read past the last counted slice
+                    if ((int64_t)tb > room) { tail = tb - (uint32_t)(room & ~(int64_t)15); tb -= tail; }
+                }
+                const uint32_t tot = __reduce_add_sync(kFull, lane <= TJ ? tb : 0u);
+                fence_proxy_async();   // this warp's earlier generic reads of the staging area come first
+                __syncwarp();
+                if (lane == 0) mbar_expect_tx(&sbar, tot);
+                __syncwarp();
+                if (lane <= TJ && tb) tma_load_1d(stg + lane * a.RB2, row_src - dl, tb, &sbar);
+                if (lane <= TJ && tail)   // the clipped end of the volume's last row: plain byte copies
+                    for (uint32_t b = tb; b < tb + tail; ++b)
+                        if ((int64_t)b < (int64_t)dl + copy_bytes) stg[lane * a.RB2 + b] = row_src[(int64_t)b - dl];
+                mbar_wait(&sbar, sph);
+                sph ^= 1u;
+                __syncwarp();
+                const uint32_t nch = (copy_bytes + 15u) >> 4;
+                for (int g = 0; g <= TJ; ++g) {
+                    const uint32_t d = __shfl_sync(kFull, dl, g);
+                    const uint32_t q = d >> 2, r = 8u * (d & 3u);
+                    const uint32_t sa = smem_u32(stg + g * a.RB2), da = smem_u32(dst + g * RB);
+                    for (uint32_t c = lane; c < nch; c += 32) {
+                        uint32_t v[8];
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(sa + 16u * c));
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "r"(sa + 16u * c + 16u));
+                        uint32_t o[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t lo = q == 0 ? v[e] : q == 1 ? v[e + 1] : q == 2 ? v[e + 2] : v[e + 3];
+                            const uint32_t hi = q == 0 ? v[e + 1] : q == 1 ? v[e + 2] : q == 2 ? v[e + 3] : v[e + 4];
+                            o[e] = __funnelshift_r(lo, hi, r);
+                        }
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(da + 16u * c), "r"(o[0]), "r"(o[1]),
+                                     "r"(o[2]), "r"(o[3]) : "memory");
+                    }
+                }
+                mbar_arrive(&full[slot]);
             } else {
                 for (int g = 0; g <= TJ; ++g) {
                     const int64_t j = min(j0 + g, N - 1);

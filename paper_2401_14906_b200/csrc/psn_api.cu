@@ -390,7 +390,7 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
         int cpl = 1;
         while (cpl < cpl_max && 32 * cpl < chunks) cpl *= 2;
         const bool use3 = ctx->count_mode == PSN_COUNT_AUTO && chunks <= 32 * cpl;
-        CountArgs ca;
+        CountArgs ca{};
         ca.labels = slab0; ca.M = L.M; ca.N = L.N; ca.O = L.O; ca.z_lo = vol->z_lo;
         ca.kA = L.kA; ca.kB = L.kB; ca.own_k0 = vol->own_k0; ca.own_k1 = vol->own_k1; ca.W32 = L.W32;
         ca.cntP = at<uint32_t>(ws, L.cntP); ca.cntQ = at<uint32_t>(ws, L.cntQ); ca.cntS = at<uint32_t>(ws, L.cntS);
@@ -413,10 +413,15 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
             // ring depth: as many slices as keep 3 CTAs resident per SM (<= ~70 KB each), 3..8
             const int64_t SBy = (int64_t)(kC3Rows + 1) * RB;
             // (a general label set also keeps its 8 KB classification bitset in shared memory)
-            const int64_t budget = 108 * 1024 - ((!anz && eb < 4) ? 8 * 1024 : 0);
+            // rows of an odd 1- / 2-byte length: a staging area for the aligned supersets (k_count3)
+            const bool shift = !ca.tma && (L.M * eb) % 4 != 0 && (reinterpret_cast<uintptr_t>(slab0) & 15u) == 0;
+            const int64_t RB2 = shift ? (int64_t)align16((size_t)(L.M * eb)) + 32 : 0;
+            const int64_t stg = (int64_t)(kC3Rows + 1) * RB2;
+            const int64_t budget = 108 * 1024 - ((!anz && eb < 4) ? 8 * 1024 : 0) - stg;
             int ns = (int)std::max<int64_t>(3, std::min<int64_t>(kC3MaxStages, budget / SBy));
-            const size_t smem = (size_t)ns * (size_t)(kC3Rows + 1) * (size_t)RB;
+            const size_t smem = (size_t)ns * (size_t)(kC3Rows + 1) * (size_t)RB + (size_t)stg;
             ca.NS = ns;
+            ca.stg_off = (int64_t)ns * SBy; ca.RB2 = RB2;
             ca.nXT = 1; ca.nJB = nJB; ca.KZ = KZ; ca.RB = RB; ca.multi_xt = 0;
             const int64_t blocks = nJB * nZC;
             if (eb == 1) ce = dispatch_count3<uint8_t>(ca, anz, cpl, blocks, smem, st);

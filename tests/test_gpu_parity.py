@@ -486,3 +486,22 @@ def test_row_width_class_boundaries(dtype):
             if dtype == np.uint32:
                 a = a * np.uint32(0x10001)
             _check_volume(a, T=2)
+
+
+@pytest.mark.parametrize("dtype,M", [(np.uint16, 257), (np.uint8, 131), (np.uint8, 262), (np.uint16, 130),
+                                     (np.uint32, 129)])
+def test_unaligned_rows_staging(dtype, M):
+    """Rows whose byte length is not a multiple of 16 (k_count3 cannot TMA them as they are): odd
+    1- / 2-byte lengths go through the aligned-superset staging + shared-memory shift, 4- / 8-byte
+    multiples through cp.async words -- several j-blocks and ring wrap-arounds, bit-exact vs the oracle."""
+    rng = np.random.default_rng(M)
+    O, N = 30, 41
+    z, y, x = np.meshgrid(np.arange(O), np.arange(N), np.arange(M), indexing="ij")
+    a = np.zeros((O, N, M), np.int64)
+    for lab in range(1, 6):
+        c = rng.uniform(0, 1, 3) * np.array([M, N, O])
+        r = rng.uniform(6, 18)
+        a[(x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2 <= r * r] = lab
+    m = rng.random(a.shape) < 0.01
+    a[m] = rng.integers(0, 6, int(m.sum()))
+    _check_volume(a.astype(dtype), T=3)
