@@ -766,7 +766,6 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     const int64_t nw = mesh->n_points;
     if (nw == 0) return PSN_OK;
     const int64_t g = grid_for(ctx, nw);
-    const int64_t gs = std::max<int64_t>(1, std::min<int64_t>((nw + 511) / 512, (int64_t)ctx->sms * 16));  // 64 points per warp
     if (iterations == 0 || relaxation == 0.f) {
         k_finalize<<<(unsigned)g, 256, 0, st>>>(nullptr, mesh->points, out, 0, nw, vol->spacing[0], vol->spacing[1],
                                                vol->spacing[2], vol->origin[0], vol->origin[1], vol->origin[2]);
