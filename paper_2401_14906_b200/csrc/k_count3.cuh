@@ -185,6 +185,10 @@ __device__ __forceinline__ uint32_t slow_chunk(uint32_t aA, uint32_t aB, uint32_
         }
     }
     uint32_t bits = 0, qacc = 0, fxc = 0, fyc = 0, fzc = 0;
+    // face / quad flag planes are packed side by side (pack<T>) and counted with one popcount per
+    // counter: EB flag positions per element slot hold NW face planes or EB/3 words of quad planes
+    constexpr int QW = Pack<T>::EB / 3;
+    uint32_t ay = 0, az = 0, ax = 0, aq = 0;
 #pragma unroll
     for (int q = 0; q < NW; ++q) {
         const uint32_t a = A[q], b = B[q], c = C[q], ha = hA[q];
@@ -195,17 +199,18 @@ __device__ __forceinline__ uint32_t slow_chunk(uint32_t aA, uint32_t aB, uint32_
         const uint32_t mv = mvox[q];
         const uint32_t pt = nz<T>(fx | fy | fz | (a ^ hD[q])) & mv;   // the 8 corners are not all one class
         bits |= movemask<T>(pt) << (q * EPW);
-        fyc += __popc(nz<T>(fy) & mv & sc.my);
-        fzc += __popc(nz<T>(fz) & mv & sc.mz);
+        ay = pack<T>(ay, nz<T>(fy) & mv & sc.my);
+        az = pack<T>(az, nz<T>(fz) & mv & sc.mz);
         if (sc.own) {
-            fxc += __popc(nz<T>(fx) & mi1[q]);
+            ax = pack<T>(ax, nz<T>(fx) & mi1[q]);
             // owned quads: x at (j>=1, k>=1), y at (i>=1, k>=1), z at (i>=1, j>=1)
-            uint32_t u = nz<T>(xa) & mv & sc.mqx;
-            u = pack<T>(u, nz<T>(yab) & mi1[q] & sc.mqy);
-            u = pack<T>(u, nz<T>(zac) & mi1[q] & sc.mqz);
-            qacc += __popc(u);
+            aq = pack<T>(aq, nz<T>(xa) & mv & sc.mqx);
+            aq = pack<T>(aq, nz<T>(yab) & mi1[q] & sc.mqy);
+            aq = pack<T>(aq, nz<T>(zac) & mi1[q] & sc.mqz);
+            if ((q + 1) % QW == 0 || q == NW - 1) { qacc += __popc(aq); aq = 0u; }
         }
     }
+    fyc = __popc(ay); fzc = __popc(az); fxc = __popc(ax);
     cq += qacc;
     cs += fxc | (fyc << 10) | (fzc << 20);
     return bits;
@@ -443,28 +448,48 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                                                          ls, cq, cs);
                 if (bits) atomicOr(&wm[r0 + ri][(c * E) >> 5], bits << ((c * E) & 31));
             }
+            if (sc.own) {   // both rows' quad counts in one word (<= 32 * 3E per round)
+                const uint32_t qq = __reduce_add_sync(kFull, ri >= 0 ? cq << (16 * ri) : 0u);
+#pragma unroll
+                for (int i = 0; i < RPW; ++i) rq[i] += (qq >> (16 * i)) & 0xFFFFu;
+            }
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                if (sc.own) rq[i] += __reduce_add_sync(kFull, ri == i ? cq : 0u);
                 const uint32_t f = __reduce_add_sync(kFull, ri == i ? cs : 0u);   // <= 32 E per field: no carry
                 rsx[i] += f & 1023u; rsy[i] += (f >> 10) & 1023u; rsz[i] += f >> 20;
             }
         }
         qt = 0;
         __syncwarp();
-        // flush the layer's rows: counts always, point planes only when non-empty
+        // flush the layer's rows: counts always, point planes only when non-empty.  The RPW (<= 2) rows'
+        // point counts share one word (a row has < 2^16 voxels) and one warp scan gives every row's
+        // total and per-word prefixes.
+        static_assert(RPW <= 2, "packed flush holds two rows");
+        uint32_t wv[RPW][WPL], xin = 0;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int q = 0; q < WPL; ++q) {
+                wv[i][q] = ((dirty >> i) & 1u) ? wm[r0 + i][lane * WPL + q] : 0u;
+                c += __popc(wv[i][q]);
+            }
+            xin |= c << (16 * i);
+        }
+        uint32_t incl = xin;
+        if (dirty) {
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += y;
+            }
+        }
+        const uint32_t tot = __shfl_sync(kFull, incl, 31), exc = incl - xin;
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             if (r0 + i >= nrows) break;
             const int64_t rr = jw + i + NV * (k - a.kA);
-            if (!((dirty >> i) & 1u)) {
-                if (lane == 0) { a.cntP[rr] = 0u; a.cntQ[rr] = 0u; a.cntS[rr] = 0u; a.cntYZ[rr] = 0u; }
-                continue;
-            }
-            uint32_t wv[WPL], cnt = 0;
-#pragma unroll
-            for (int q = 0; q < WPL; ++q) { wv[q] = wm[r0 + i][lane * WPL + q]; cnt += __popc(wv[q]); }
-            const uint32_t P = __reduce_add_sync(kFull, cnt);
+            const uint32_t P = (tot >> (16 * i)) & 0xFFFFu;
             if (lane == 0) {   // S without the +y / +z faces (the scan adds rows j+1 / k+1's y / z counts)
                 a.cntP[rr] = P; a.cntQ[rr] = rq[i];
                 a.cntS[rr] = sc.own ? 2u * rsx[i] + rsy[i] + rsz[i] : 0u;
@@ -476,31 +501,27 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
                 uint32_t lo = 0xFFFFFFFFu, hi = 0u;
 #pragma unroll
                 for (int q = WPL - 1; q >= 0; --q)
-                    if (wv[q]) lo = 32u * (uint32_t)(lane * WPL + q) + (uint32_t)(__ffs(wv[q]) - 1);
+                    if (wv[i][q]) lo = 32u * (uint32_t)(lane * WPL + q) + (uint32_t)(__ffs(wv[i][q]) - 1);
 #pragma unroll
                 for (int q = 0; q < WPL; ++q)
-                    if (wv[q]) hi = 32u * (uint32_t)(lane * WPL + q) + (uint32_t)(32 - __clz(wv[q]));
+                    if (wv[i][q]) hi = 32u * (uint32_t)(lane * WPL + q) + (uint32_t)(32 - __clz(wv[i][q]));
                 lo = __reduce_min_sync(kFull, lo);
                 hi = __reduce_max_sync(kFull, hi);
                 if (lane == 0) a.trim[rr] = make_int2((int)lo, (int)hi);
-                uint32_t incl = cnt;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(kFull, incl, d);
-                    if (lane >= d) incl += y;
-                }
-                uint32_t pre = incl - cnt;
+                uint32_t pre = (exc >> (16 * i)) & 0xFFFFu;
                 uint32_t *pm = a.pmask + rr * W32;
                 uint16_t *pp = a.ppre + rr * W32;
 #pragma unroll
                 for (int q = 0; q < WPL; ++q) {
                     const int wi = lane * WPL + q;
-                    if (wi < W32) { pm[wi] = wv[q]; pp[wi] = (uint16_t)pre; }
-                    pre += __popc(wv[q]);
+                    if (wi < W32) { pm[wi] = wv[i][q]; pp[wi] = (uint16_t)pre; }
+                    pre += __popc(wv[i][q]);
                 }
             }
+            if ((dirty >> i) & 1u) {
 #pragma unroll
-            for (int q = 0; q < WPL; ++q) wm[r0 + i][lane * WPL + q] = 0u;
+                for (int q = 0; q < WPL; ++q) wm[r0 + i][lane * WPL + q] = 0u;
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot0]);   // slice o is no longer read by this warp
