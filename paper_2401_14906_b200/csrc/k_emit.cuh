@@ -439,6 +439,9 @@ __global__ void __launch_bounds__(256) k_emit_fast(EmitArgs a) {
 #endif
 constexpr int kBand = PSN_BAND_ROWS;
 constexpr int kBandThreads = 256;
+#ifndef PSN_EMIT_MINB
+#define PSN_EMIT_MINB 3   // resident CTAs per SM the register budget is sized for
+#endif
 #ifndef PSN_BAND_BUFS
 #define PSN_BAND_BUFS 2
 #endif
@@ -461,7 +464,7 @@ static_assert(sizeof(uint32_t) * kRangeCap % 16 == 0 && sizeof(uint16_t) * kRang
               "staged arrays must start at 16-byte boundaries");
 
 template <typename T, bool ANZ, int WC = 0>   // WC: plane words per row as a compile-time constant (0 = a.W32)
-__global__ void __launch_bounds__(kBandThreads, 3) k_emit_band(EmitArgs a) {
+__global__ void __launch_bounds__(kBandThreads, PSN_EMIT_MINB) k_emit_band(EmitArgs a) {
     constexpr int B = kBand;
     extern __shared__ __align__(128) uint8_t dsm_band[];
     BandBuf *buf = reinterpret_cast<BandBuf *>(dsm_band);   // [kBandBufs]
