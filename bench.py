@@ -566,7 +566,7 @@ def main():
                     help="N = 1: call the library per step instead of replaying the step's CUDA graphs")
     ap.add_argument("--smooth-cache", action="store_true",
                     help="N = 1: the emission writes the packed smoothing cache next to the stencils and psn_smooth "
-                         "skips k_smooth_prep8 (measured: c4 step -0.2 %, extraction +3 %; c5a step -1.6 %)")
+                         "skips k_smooth_prep8 (measured: c4 step -0.2 %%, extraction +3 %%; c5a step -1.6 %%)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="cpu_baseline: repeat the reference arm's sample window until this much CPU time")
