@@ -267,6 +267,7 @@ class PSN:
             dims = (M, N, Z)
         v = Volume()
         v.labels = labels.data_ptr()
+        v._keep = labels   # the struct holds a raw device pointer: keep the tensor alive with it
         v.dtype = _DTYPES[labels.dtype]
         for a in range(3):
             v.dims[a] = int(dims[a]); v.spacing[a] = float(spacing[a]); v.origin[a] = float(origin[a])

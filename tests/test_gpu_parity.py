@@ -505,3 +505,21 @@ def test_unaligned_rows_staging(dtype, M):
     m = rng.random(a.shape) < 0.01
     a[m] = rng.integers(0, 6, int(m.sum()))
     _check_volume(a.astype(dtype), T=3)
+
+
+def test_volume_keeps_its_labels_alive():
+    """PSN.volume holds the label tensor: a volume built from a temporary stays valid after the
+    temporary's last Python reference is dropped and its memory would otherwise be reused."""
+    import gc
+    rng = np.random.default_rng(11)
+    a = rng.integers(0, 3, size=(20, 24, 28)).astype(np.uint16)
+    p = gu.psn()
+    vol = p.volume(torch.from_numpy(a).cuda())   # no other reference to the device tensor
+    gc.collect()
+    junk = torch.full((4 << 20,), 0x5A5A, dtype=torch.int32, device="cuda")   # would overwrite freed memory
+    mesh = p.extract(vol)
+    torch.cuda.synchronize()
+    om = oracle.extract(oracle.as_volume(a))
+    assert (mesh.n_points, mesh.n_quads, mesh.n_stencil) == (om.n_points, om.n_quads, om.n_stencil)
+    assert np.array_equal(gu.u32(mesh.quads, mesh.n_quads), om.quads)
+    del junk
