@@ -301,11 +301,21 @@ def run_psn(args, rank, world, local_rank):
             pipe.run()
             # the smoothing graph records two events around its T Jacobi launches (psn_ctx_set_smooth_events):
             # k_smooth_v4's mean launch time for the roofline, replayed back to back as in the timed steps
-            sm_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-            psn.set_smooth_events(sm_ev)
             pipe.capture()
-            psn.set_smooth_events(None)
             run_extract, run_smooth = pipe.replay_extract, pipe.replay_smooth
+            # one smoothing graph per timed step, each recording its own event pair around the T Jacobi
+            # launches: the roofline's launch time is the mean over ALL timed steps (a single step's pair
+            # picked up one slow replay in some runs)
+            sm_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+            sm_graphs = []
+            for e2 in sm_ev:
+                psn.set_smooth_events(e2)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    pipe.smooth()
+                sm_graphs.append(g)
+            psn.set_smooth_events(None)
+            torch.cuda.synchronize()
     else:
         from paper_2401_14906_b200.dist import (SlabPipeline, balanced_layer_cuts, gather_layer_points,
                                                 partition, slab_slices)
@@ -384,14 +394,17 @@ def run_psn(args, rank, world, local_rank):
         ev[s][0].record(stream)
         run_extract()
         ev[s][1].record(stream)
-        run_smooth()
+        if graphs:
+            sm_graphs[s].replay()   # the step's own smoothing graph (same kernels, its own event pair)
+        else:
+            run_smooth()
         ev[s][2].record(stream)
     torch.cuda.synchronize()
     clk.mark(False)
     psn.set_pass_events(None)
-    # k_smooth_v4 launch time inside the timed region: the captured smoothing graph recorded two events
-    # around its T Jacobi launches in every replay; they now hold the last timed step's
-    t_v4_live = sm_ev[0].elapsed_time(sm_ev[1]) / T if (graphs and T > 0) else None
+    # Jacobi launch time inside the timed region: every timed step's smoothing graph recorded two events
+    # around its T launches; the mean over the K timed steps
+    t_v4_live = (sum(e2[0].elapsed_time(e2[1]) for e2 in sm_ev) / len(sm_ev) / T) if (graphs and T > 0) else None
     if graphs:   # per-pass times from K direct (non-graph) extractions: the pass events are host calls
         for s in range(K):
             if flush is not None:
@@ -441,17 +454,21 @@ def run_psn(args, rank, world, local_rank):
     per_launch_ms = t_v4 if t_v4 else t_sm / max(T, 1)
     sm_gbs = b_sm / (t_sm / max(T, 1) * 1e-3) / 1e9          # the smoothing half incl. the cache prep
     v4_gbs = b_sm / (per_launch_ms * 1e-3) / 1e9
-    dominant = "k_smooth_v4" if t_sm >= t_ext else "extraction (k_count3+k_scan+k_emit_band)"
-    roof = {"bound": "hbm", "kernel": "k_smooth_v4", "achieved": v4_gbs / world, "peak": peak, "unit": "GB/s",
-            "frac": v4_gbs / world / peak, "traffic": profile_traffic("k_smooth_v4", cfg), "peak_source": peak_src,
+    # whole-volume psn_smooth (N = 1): iteration 1 is k_smooth_v4, iterations 2..T k_smooth_split (split cache);
+    # slabs / shards (N > 1) step with k_smooth_v4
+    sm_kern = "k_smooth_split" if (world == 1 and T > 1) else "k_smooth_v4"
+    dominant = sm_kern if t_sm >= t_ext else "extraction (k_count3+k_scan+k_emit_band)"
+    roof = {"bound": "hbm", "kernel": sm_kern, "achieved": v4_gbs / world, "peak": peak, "unit": "GB/s",
+            "frac": v4_gbs / world / peak, "traffic": profile_traffic(sm_kern, cfg), "peak_source": peak_src,
             "bytes_per_launch": b_sm / world, "launch_ms": per_launch_ms,
-            "note": ("achieved = algorithmic bytes per launch (24P + 4(P+1) + 4S, per GPU) / average k_smooth_v4 launch "
+            "note": ("achieved = algorithmic bytes per launch (24P + 4(P+1) + 4S, per GPU) / average Jacobi launch "
                      "time: CUDA events the library records around the T back-to-back Jacobi launches of psn_smooth "
-                     "(psn_ctx_set_smooth_events; the one-off cache prep excluded), recorded by the captured smoothing "
-                     "graph in the last timed step (K direct calls after the timed region with --no-graph), divided by T")
+                     "(psn_ctx_set_smooth_events; iteration 1 also builds the smoothing cache, k_smooth_first), "
+                     "recorded by each timed step's captured smoothing graph and averaged over the K timed steps "
+                     "(K direct calls after the timed region with --no-graph), divided by T")
                     if t_v4 else
                     ("achieved = algorithmic bytes per launch / (smoothing half incl. the one-off cache prep) / T")}
-    if dominant != "k_smooth_v4":
+    if dominant != sm_kern:
         roof["note"] += "; extraction dominated this config's step, see extract.frac"
 
     # per-pass roofline (SURVEY 8(d) per-kernel byte budgets, per GPU): counting reads the labels once,

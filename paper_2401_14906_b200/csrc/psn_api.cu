@@ -187,6 +187,11 @@ template <bool PK, bool PF, bool PE> V4Fn v4_sel(bool sphere) {
     return sphere ? k_smooth_v4<PK, PF, PE, true> : k_smooth_v4<PK, PF, PE, false>;
 }
 
+V4Fn split_sel(bool pref, bool sphere) {
+    if (pref) return sphere ? k_smooth_split<true, true> : k_smooth_split<true, false>;
+    return sphere ? k_smooth_split<false, true> : k_smooth_split<false, false>;
+}
+
 template <typename T, bool ANZ, int CPL, int RPW, bool FULL, bool EXACT>
 cudaError_t launch_count3_f(const CountArgs &ca, int64_t blocks, size_t smem, cudaStream_t st) {
     static size_t attr_set = 0;
@@ -776,7 +781,12 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
     const bool packed = ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION && smooth_packed(ctx, vol);
     // the packed cache written by the emission, if any, replaces the prep pass
     const bool cached = packed && mesh->smooth_cache && mesh->smooth_cache_valid;
-    if (!cached && (s = packed ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st)) != PSN_OK) return s;
+    // split cache without an emitted cache: the first iteration builds it (k_smooth_first, no prep pass)
+    const size_t hi_at = align_up(8 * (size_t)nw);
+    const bool split = packed && iterations > 1 && hi_at + 4 * (size_t)nw <= SL.buf0 && !getenv("PSN_SMOOTH_NOSPLIT");
+    const bool first = split && !cached && !getenv("PSN_SMOOTH_NOFIRST");
+    if (!cached && !first && (s = packed ? launch_prep8(ctx, mesh, ws, st) : launch_prep(ctx, mesh, ws, st)) != PSN_OK)
+        return s;
     if (ctx->smooth_mode == PSN_SMOOTH_PER_ITERATION) {
         // one launch per Jacobi iteration, offsets double-buffered in the two buffer slots
         SmoothV4 v = smooth_v4_args(ctx, vol, mesh, ws, relaxation, constraint_distance);
@@ -785,14 +795,29 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         // one-step-ahead cache loads: measured faster up to tens of millions of points (c6
         // -8 %, c4 -3 %) and slower on c5a's 133 M (+8 %), where the step is closest to the
         // DRAM bound; chosen by size
-        const V4Fn kern = pick_v4(packed, packed && nw < (1ll << 26), false, cons.sphere != 0);
+        const bool pref = packed && nw < (1ll << 26);
+        const V4Fn kern = pick_v4(packed, pref, false, cons.sphere != 0);
         const int64_t g4 = v4_grid(ctx, kern, nw);
+        // split cache (k_smooth_split): iterations 2..T take the cache entry's lo word from the w slot of
+        // the point's own offsets and its hi word from a 4-byte array in the cache region's second half
+        // (free: the packed cache uses 8 of the 16 bytes per point the region holds)
+        uint32_t *hi = split ? at<uint32_t>(ws, hi_at) : nullptr;
+        const V4Fn kern2 = split ? split_sel(pref && !getenv("PSN_SPLIT_NOPREF"), cons.sphere != 0) : kern;
+        const int64_t g42 = split ? v4_grid(ctx, kern2, nw) : g4;
         const float4 *s4 = nullptr;
         if (ctx->smooth_ev[0]) record_event(ctx->smooth_ev[0], st);
         for (int32_t t = 0; t < iterations; ++t) {
             const bool last = (t == iterations - 1);
             v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
-            kern<<<(unsigned)g4, 256, 0, st>>>(v);
+            v.hi_out = (split && t == 0) ? hi : nullptr; v.hi = hi;
+            if (t == 0 && first) {
+                v.fmask = mesh->face_masks; v.csr_off = mesh->stencil_offsets; v.csr_ids = mesh->stencil_ids;
+                v.win_base = (uint32_t)(mesh->first_point - mesh->halo_lo_points);
+                v.first_stencil = (uint32_t)mesh->first_stencil;
+                if (cons.sphere) k_smooth_first<true><<<(unsigned)grid_for(ctx, nw), 256, 0, st>>>(v);
+                else k_smooth_first<false><<<(unsigned)grid_for(ctx, nw), 256, 0, st>>>(v);
+            } else if (t == 0) kern<<<(unsigned)g4, 256, 0, st>>>(v);
+            else kern2<<<(unsigned)g42, 256, 0, st>>>(v);
             ++ctx->launches;
             s4 = v.dst;
         }

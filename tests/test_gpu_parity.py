@@ -343,6 +343,47 @@ def test_packed_smoothing_cache_bit_identical(monkeypatch):
         assert torch.equal(built, mesh.smooth_cache[:n])
 
 
+@pytest.mark.parametrize("sphere", [0, 1])
+def test_split_smoothing_cache_bit_identical(monkeypatch, sphere):
+    """Iterations 2..T with the split cache (k_smooth_split: the packed entry's lo word in the
+    offsets' w slot, the hi word in a 4-byte array) give the same bits as k_smooth_v4 reading
+    the 8-byte entries every iteration -- emitted cache, prep-built cache, and the cache built
+    by the first iteration itself (k_smooth_first); T = 1, 2, 3, 9, box and sphere constraints,
+    and a mesh too small for the split (it falls back)."""
+    p = gu.psn()
+    rng = np.random.default_rng(91)
+    vols = [rng.integers(0, 4, size=(12, 40, 60)).astype(np.uint8),
+            psn_gen.generate_host(psn_gen.config("c2"))[96:150],
+            np.pad(np.ones((1, 1, 1), np.uint16), 1)]
+    p.set_constraint(sphere)
+    try:
+        for a in vols:
+            dev = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            vol = p.volume(dev, spacing=(0.8, 1.0, 1.5))
+            labels, ws_e = p.labels(None), p.workspace(vol)
+            counted = p.count(vol, labels, ws_e)
+            mesh = p.alloc_mesh(counted.n_points, counted.n_points, counted.n_quads, counted.n_stencil,
+                                smooth_cache=True)
+            mesh = p.emit(vol, labels, ws_e, counted, mesh=mesh)
+            ws = p.smooth_workspace(mesh)
+            n = mesh.n_points
+            for T in (1, 2, 3, 9):
+                for cached in (1, 0):
+                    mesh.c.smooth_cache_valid = cached
+                    split = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()   # cached=0: k_smooth_first
+                    monkeypatch.setenv("PSN_SMOOTH_NOFIRST", "1")
+                    split_prep = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()   # k_smooth_prep8 + split
+                    monkeypatch.delenv("PSN_SMOOTH_NOFIRST")
+                    monkeypatch.setenv("PSN_SMOOTH_NOSPLIT", "1")
+                    plain = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws)
+                    monkeypatch.delenv("PSN_SMOOTH_NOSPLIT")
+                    assert torch.equal(split[:n], plain[:n]), (a.shape, T, cached)
+                    assert torch.equal(split_prep[:n], plain[:n]), (a.shape, T, cached)
+                mesh.c.smooth_cache_valid = 1
+    finally:
+        p.set_constraint(0)
+
+
 def test_dense_wide_rows_and_layers_smoothing():
     """Dense iid volumes whose rows hold ~1400 points and whose layers hold ~600K points, so
     stencil neighbours are far apart in id space: extraction and smoothing still match the oracle."""
