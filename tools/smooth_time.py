@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--graph", action="store_true", help="replay psn_smooth captured in a CUDA graph (as bench.py)")
     a = ap.parse_args()
     spec = psn_gen.config(a.config)
     T, lam, d = psn_gen.SMOOTHING[a.config]
@@ -29,11 +30,19 @@ def main():
     pipe.run()
     for _ in range(2):
         pipe.smooth()
+    run = pipe.smooth
+    if a.graph:
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            pipe.smooth()
+        run = g.replay
+        run()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     s.record()
     for _ in range(a.reps):
-        pipe.smooth()
+        run()
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / a.reps
@@ -41,7 +50,7 @@ def main():
     x = pipe.out[:P].contiguous().view(torch.int32).to(torch.int64)
     dig = int((x * torch.arange(1, x.numel() + 1, device=x.device).view(x.shape)).sum()) % (1 << 61)
     print(json.dumps({"config": a.config, "lib": os.path.basename(os.environ.get("PSN_LIB", "default")), "P": P,
-                      "T": T, "smooth_ms": ms, "per_iter_us": 1e3 * ms / T, "digest": dig}), flush=True)
+                      "T": T, "graph": a.graph, "smooth_ms": ms, "per_iter_us": 1e3 * ms / T, "digest": dig}), flush=True)
 
 
 if __name__ == "__main__":
