@@ -36,6 +36,7 @@ struct EmitArgs {
     const int64_t *first_dev;  // if non-NULL: the global first ids (point, quad, stencil) in device memory
     ScanHeader *hdr;
     uint2 *scache;             // if non-NULL (k_emit_band): packed smoothing cache of the own points
+    int dual;                  // k_emit_band: both density variants launched, each returns unless selected
 };
 
 __device__ __forceinline__ float anchor_coord(double org, double sp, int64_t idx) {
@@ -450,7 +451,10 @@ constexpr int kBandBufs = PSN_BAND_BUFS;   // staged bands per CTA (ring; 2 keep
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-constexpr uint32_t kStageCsr = 150;   // rounds with >= this many CSR ids write them through shared memory
+#ifndef PSN_STAGE_CSR
+#define PSN_STAGE_CSR 150
+#endif
+constexpr uint32_t kStageCsr = PSN_STAGE_CSR;   // rounds with >= this many CSR ids write them through shared memory
 
 constexpr int kRangeCap = (kBand + 2) * 32 + 16;   // elements per staged range (+ alignment slack)
 struct BandBuf {                      // one stage; word / prefix ranges keep the workspace's row stride W32
@@ -463,7 +467,12 @@ static_assert(sizeof(uint32_t) * kRangeCap % 16 == 0 && sizeof(uint16_t) * kRang
               sizeof(uint32_t) * (kBand + 12) % 16 == 0 && sizeof(uint32_t) * (kBand + 8) % 16 == 0,
               "staged arrays must start at 16-byte boundaries");
 
-template <typename T, bool ANZ, int WC = 0>   // WC: plane words per row as a compile-time constant (0 = a.W32)
+// WC: plane words per row as a compile-time constant (0 = a.W32).  STG: dense rounds write their points
+// and CSR ids through shared memory (meshes with >= kStageCsr / 32 stencil entries per point, e.g. c5a);
+// without it 6 KB per CTA more go to L1 (c4 emission -2.6 %).  Both variants give the same bits.  The
+// host launches the one for the density of the last mesh whose totals it read; when it has read none
+// (a.dual), both are launched back to back and each returns at once unless the scan totals select it.
+template <typename T, bool ANZ, int WC = 0, bool STG = true>
 __global__ void __launch_bounds__(kBandThreads, PSN_EMIT_MINB) k_emit_band(EmitArgs a) {
     constexpr int B = kBand;
     extern __shared__ __align__(128) uint8_t dsm_band[];
@@ -472,7 +481,7 @@ __global__ void __launch_bounds__(kBandThreads, PSN_EMIT_MINB) k_emit_band(EmitA
     __shared__ int32_t s_band[kBandBufs];   // band staged in each buffer (nbands: end of the CTA's list)
     __shared__ uint32_t s_done[kBandBufs];  // warps finished with each buffer
     __shared__ uint32_t sbits[ANZ ? 1 : 2048];
-    __shared__ uint32_t scsr[kBandThreads / 32][6 * 32];   // a round's CSR ids, written out coalesced
+    __shared__ uint32_t scsr[kBandThreads / 32][STG ? 6 * 32 : 1];   // a round's CSR ids, written out coalesced
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     LabelSet ls = a.ls;
     if (!ANZ && sizeof(T) < 4) {
@@ -489,6 +498,7 @@ __global__ void __launch_bounds__(kBandThreads, PSN_EMIT_MINB) k_emit_band(EmitA
         a.first_stencil = (uint32_t)a.first_dev[2];
     }
     const uint64_t totP = a.hdr->total[0], totQ = a.hdr->total[1], totS = a.hdr->total[2];
+    if (a.dual && (32u * totS >= (uint64_t)kStageCsr * totP) != STG) return;   // the other variant's mesh
     const uint32_t halo_lo = (uint32_t)a.hdr->halo_lo;
     if (totP > (uint64_t)a.cap_points || totQ > (uint64_t)a.cap_quads || totS > (uint64_t)a.cap_stencil) {
         if (blockIdx.x == 0 && tid == 0) a.hdr->emit_status = 1u;
@@ -769,7 +779,7 @@ __global__ void __launch_bounds__(kBandThreads, PSN_EMIT_MINB) k_emit_band(EmitA
             const uint32_t x = scan3(packed, lane);
             const uint32_t tot = __shfl_sync(kFull, x, 31);
             const uint32_t ex = x - packed;
-            const bool stage = (tot & 0xffffu) >= kStageCsr;   // dense round: CSR ids through shared memory
+            const bool stage = STG && (tot & 0xffffu) >= kStageCsr;   // dense round: CSR ids through shared memory
             if (!stage) {
                 if (act) {
                     a.points[3 * (size_t)wi + 0] = anchor_coord(a.org[0], a.sp[0], i);

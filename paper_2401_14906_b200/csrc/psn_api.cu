@@ -44,6 +44,7 @@ struct psn_ctx {
     int32_t smooth_tile = 0;                  // points per wavefront tile (0 = automatic)
     int count_mode = PSN_COUNT_AUTO;          // psn_ctx_set_counting
     int emit_mode = PSN_EMIT_AUTO;            // psn_ctx_set_emission
+    int emit_dense = -1;                      // stencil density of the last totals read back (k_emit_band STG); -1 unknown
     int constraint = PSN_CONSTRAINT_BOX;      // psn_ctx_set_constraint
     std::map<void *, void *> ipc_bases;       // psn_ipc_open: returned pointer -> mapped base
     cudaEvent_t pass_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // psn_ctx_set_pass_events
@@ -244,14 +245,27 @@ cudaError_t dispatch_count(const CountArgs &ca, bool anz, int64_t blocks, int th
 }
 
 template <typename T>
-void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st, int emit_mode) {
+void dispatch_emit(const EmitArgs &ea, bool anz, bool fast, int64_t blocks, cudaStream_t st, int emit_mode, int dense) {
     if (fast && ea.W32 <= 32 && emit_mode == 0) {   // band-staged: shared-memory id lookups
         // the row-width classes of the common volumes (M <= 1025: 32 plane words; M <= 513: 16) get the word
         // count as a compile-time constant (c4 emission -6 %, c3 -7 %, c6 -7 %)
-        if (anz && ea.W32 == 32) k_emit_band<T, true, 32><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
-        else if (anz && ea.W32 == 16) k_emit_band<T, true, 16><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
-        else if (anz) k_emit_band<T, true><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
-        else k_emit_band<T, false><<<(unsigned)blocks, kBandThreads, kBandBufs * sizeof(BandBuf), st>>>(ea);
+        // density variants (STG): the one the host's last read totals select, or both back to back (ea.dual:
+        // each kernel checks the scan totals on entry and only the selected one does the work)
+        const size_t sm = kBandBufs * sizeof(BandBuf);
+        const bool sparse = ea.dual || dense == 0, dense_ = ea.dual || dense == 1;
+        if (anz && ea.W32 == 32) {
+            if (sparse) k_emit_band<T, true, 32, false><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+            if (dense_) k_emit_band<T, true, 32, true><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+        } else if (anz && ea.W32 == 16) {
+            if (sparse) k_emit_band<T, true, 16, false><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+            if (dense_) k_emit_band<T, true, 16, true><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+        } else if (anz) {
+            if (sparse) k_emit_band<T, true, 0, false><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+            if (dense_) k_emit_band<T, true, 0, true><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+        } else {
+            if (sparse) k_emit_band<T, false, 0, false><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+            if (dense_) k_emit_band<T, false, 0, true><<<(unsigned)blocks, kBandThreads, sm, st>>>(ea);
+        }
     } else if (fast) {   // rows fit one k_count x-tile: per-word point prefixes are row prefixes
         if (anz) k_emit_fast<T, true><<<(unsigned)blocks, 256, 0, st>>>(ea);
         else k_emit_fast<T, false><<<(unsigned)blocks, 256, 0, st>>>(ea);
@@ -280,6 +294,7 @@ psn_status read_totals(psn_ctx *ctx, const psn_volume *v, const Layout &L, const
     mesh->n_quads = (int64_t)h.total[1];
     mesh->n_stencil = (int64_t)h.total[2];
     if (emit_status) *emit_status = h.emit_status;
+    ctx->emit_dense = (32u * h.total[2] >= (uint64_t)kStageCsr * h.total[0]) ? 1 : 0;
     const uint64_t lim = 1ull << 32;
     if (h.total[0] >= lim || h.total[1] >= lim || h.total[2] >= lim)
         return fail(ctx, PSN_ERR_OVERFLOW, "output exceeds 32-bit ids: P=%llu Q=%llu S=%llu",
@@ -541,6 +556,13 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
                                   (const void *)k_emit_band<uint16_t, true, 32>, (const void *)k_emit_band<uint16_t, true, 16>,
                                   (const void *)k_emit_band<uint32_t, true, 32>, (const void *)k_emit_band<uint32_t, true, 16>})
                 cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBandBufs * sizeof(BandBuf)));
+            for (const void *f : {(const void *)k_emit_band<uint8_t, true, 0, false>, (const void *)k_emit_band<uint8_t, false, 0, false>,
+                                  (const void *)k_emit_band<uint16_t, true, 0, false>, (const void *)k_emit_band<uint16_t, false, 0, false>,
+                                  (const void *)k_emit_band<uint32_t, true, 0, false>, (const void *)k_emit_band<uint32_t, false, 0, false>,
+                                  (const void *)k_emit_band<uint8_t, true, 32, false>, (const void *)k_emit_band<uint8_t, true, 16, false>,
+                                  (const void *)k_emit_band<uint16_t, true, 32, false>, (const void *)k_emit_band<uint16_t, true, 16, false>,
+                                  (const void *)k_emit_band<uint32_t, true, 32, false>, (const void *)k_emit_band<uint32_t, true, 16, false>})
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBandBufs * sizeof(BandBuf)));
             attr = true;
         }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBandThreads, kBandBufs * sizeof(BandBuf));
@@ -548,10 +570,14 @@ psn_status psn_extract(psn_ctx *ctx, const psn_volume *vol, const psn_labels *la
     }
     const bool fast = emode != PSN_EMIT_SCAN &&
                       (L.M - 1) <= (int64_t)(eb == 1 ? count_xt<uint8_t>() : eb == 2 ? count_xt<uint16_t>() : count_xt<uint32_t>());
-    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, fast, blocks, st, emode);
-    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st, emode);
-    else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st, emode);
-    ++ctx->launches;
+    const bool band = fast && L.W32 <= 32 && emode == 0;
+    const char *dv = getenv("PSN_EMIT_DENSE");   // test / A-B override: -1 both, 0 sparse, 1 dense variant
+    const int dense = dv ? atoi(dv) : ctx->emit_dense;
+    ea.dual = (band && dense < 0) ? 1 : 0;   // density unknown to the host: both variants
+    if (eb == 1) dispatch_emit<uint8_t>(ea, anz, fast, blocks, st, emode, dense);
+    else if (eb == 2) dispatch_emit<uint16_t>(ea, anz, fast, blocks, st, emode, dense);
+    else dispatch_emit<uint32_t>(ea, anz, fast, blocks, st, emode, dense);
+    ctx->launches += ea.dual ? 2 : 1;
     pass_mark(ctx, 3, st);
     return cuda_check(ctx, "emit launch");
 }

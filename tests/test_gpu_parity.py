@@ -98,6 +98,21 @@ def test_random_corpus_bit_exact(counting, emission):
         p.set_emission(0)
 
 
+@pytest.mark.parametrize("dense", ["-1", "0", "1"])
+def test_emission_density_variants_bit_exact(monkeypatch, dense):
+    """k_emit_band's two density variants (STG: dense rounds staged through shared memory, or not)
+    and the dual launch (both variants, the scan totals pick one on the device) reproduce the
+    oracle bit for bit on sparse and dense (i.i.d., > 4.7 stencil entries per point) meshes,
+    whichever the host selects -- including the wrong one for the mesh's density."""
+    monkeypatch.setenv("PSN_EMIT_DENSE", dense)
+    rng = np.random.default_rng(5150)
+    for a, ls in _corpus(rng, 24):
+        _check_volume(a, ls, spacing=(0.8, 1.0, 1.5), origin=(-3.0, 2.0, 10.0), T=2)
+    iid = rng.integers(0, 4, size=(20, 37, 131)).astype(np.uint8)
+    mesh = _check_volume(iid, T=2)
+    assert mesh.n_stencil * 32 >= 150 * mesh.n_points   # dense: the staging variant's case
+
+
 def test_two_by_two_by_two_exhaustive():
     """All 2^8 binary and 3^8 ternary 2x2x2 volumes in one batch each (as slabs of one volume
     would mix them; here each is its own call through the ABI)."""
