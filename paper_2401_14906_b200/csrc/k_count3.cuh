@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
         }
         qt = 0;
         __syncwarp();
+        // slice o is no longer read (the flush below reads wm and registers only): release its slot before
+        // the flush, so the producer refills it sooner (c4 count -1.7 %)
+        if (lane == 0) mbar_arrive(&empty[slot0]);
         // flush the layer's rows: counts always, point planes only when non-empty.  The RPW (<= 2) rows'
         // point counts share one word (a row has < 2^16 voxels) and one warp scan gives every row's
         // total and per-word prefixes.
@@ -524,7 +527,6 @@ __global__ void __launch_bounds__(32 * (kC3Rows / RPW + 1)) k_count3(CountArgs a
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot0]);   // slice o is no longer read by this warp
         slot0 = slot1;
         if (++slot1 == NS) { slot1 = 0; ph1 ^= 1u; }
 #pragma unroll

@@ -35,7 +35,7 @@ def volume(rng):
         a = np.zeros((O, N, M), np.int64)
         for lab in range(1, int(rng.integers(2, 9))):
             c = rng.uniform(0, 1, 3) * np.array([M, N, O])
-            r = rng.uniform(1.5, 0.6 * max(M, N, O))
+            r = rng.uniform(1.5, max(1.6, 0.6 * max(M, N, O)))
             a[(x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2 <= r * r] = lab
         if kind == 2:
             m = rng.random(a.shape) < 0.05
