@@ -444,10 +444,17 @@ __global__ void __launch_bounds__(256) k_smooth_split(SmoothV4 a) {
 template <bool SPHERE>
 __global__ void __launch_bounds__(256) k_smooth_first(SmoothV4 a) {
     const float3 z = make_float3(0.f, 0.f, 0.f);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_own; i += gridDim.x * blockDim.x) {
-        const uint32_t fm = a.fmask[i];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    // face mask and CSR offset of the next grid-stride step loaded one step ahead: only the stencil-id
+    // loads stay on a step's dependent chain (one resident wave of CTAs; c4 smoothing -1.0 %, c3 -1.4 %)
+    uint32_t fm_n = 0u, so_n = 0u;
+    if (i < a.n_own) { fm_n = a.fmask[i]; so_n = __ldg(a.csr_off + i); }
+    for (; i < a.n_own; i += stride) {
+        const uint32_t fm = fm_n;
+        uint32_t s = so_n - a.first_stencil;
+        if (i + stride < a.n_own) { fm_n = a.fmask[i + stride]; so_n = __ldg(a.csr_off + i + stride); }
         const uint32_t w = a.halo_lo + i;
-        uint32_t s = __ldg(a.csr_off + i) - a.first_stencil;
         uint4 v = make_uint4(w, w, w, w);
         if (fm & 1u) v.x = __ldg(a.csr_ids + s++) - a.win_base;    // -z
         if (fm & 2u) v.y = __ldg(a.csr_ids + s++) - a.win_base;    // -y

@@ -840,8 +840,9 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
                 v.fmask = mesh->face_masks; v.csr_off = mesh->stencil_offsets; v.csr_ids = mesh->stencil_ids;
                 v.win_base = (uint32_t)(mesh->first_point - mesh->halo_lo_points);
                 v.first_stencil = (uint32_t)mesh->first_stencil;
-                if (cons.sphere) k_smooth_first<true><<<(unsigned)grid_for(ctx, nw), 256, 0, st>>>(v);
-                else k_smooth_first<false><<<(unsigned)grid_for(ctx, nw), 256, 0, st>>>(v);
+                const int64_t gf = v4_grid(ctx, cons.sphere ? k_smooth_first<true> : k_smooth_first<false>, nw);
+                if (cons.sphere) k_smooth_first<true><<<(unsigned)gf, 256, 0, st>>>(v);
+                else k_smooth_first<false><<<(unsigned)gf, 256, 0, st>>>(v);
             } else if (t == 0) kern<<<(unsigned)g4, 256, 0, st>>>(v);
             else kern2<<<(unsigned)g42, 256, 0, st>>>(v);
             ++ctx->launches;
