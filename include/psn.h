@@ -368,7 +368,12 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
  * every rank would otherwise run around psn_smooth_step_peer.  The result is in
  * buf[(peer->iteration - 1) & 1] (peer->iteration as updated by the call).
  * Continuing the parity across calls keeps a later run's first push out of
- * the buffer a neighbour's previous run ended in. */
+ * the buffer a neighbour's previous run ended in.  With the packed cache and
+ * iterations > 1 the run uses the split cache (as psn_smooth): step 0 writes
+ * the hi words of the packed entries into the unused second half of the
+ * cache region of `ws` (scratch of this call; the prepared cache itself is
+ * not modified) and the lo words into the w slots of the offsets, steps
+ * 1.. read them -- bit-identical to the 8-byte-cache steps. */
 psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
                                size_t ws_bytes, float *buf0, float *buf1, int32_t iterations, float relaxation,
                                float constraint_distance, psn_peer *peer, void *stream);

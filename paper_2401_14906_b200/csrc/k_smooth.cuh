@@ -266,27 +266,51 @@ __device__ __forceinline__ float4 ld_src(const float4 *p) {
     else return __ldg(p);
 }
 
+// Peer step prologue: both neighbours finished iteration g - 1 (their halo pushes are here).
+__device__ __forceinline__ void peer_wait(const SmoothV4 &a) {
+    if (threadIdx.x == 0) {
+        const uint64_t t0 = globaltimer_ns();
+        for (int s = 0; s < 2; ++s) {
+            if (!a.peer.side[s].dst) continue;
+            while (ld_acquire_sys64(a.peer.sig + s) < a.peer.g) {
+                if (globaltimer_ns() - t0 > kPeerTimeoutNs) {   // fail loudly: no smoothing on stale halos
+                    atomicExch(a.peer.err, 1u);
+                    __threadfence_system();
+                    __trap();
+                }
+                __nanosleep(64);
+            }
+        }
+    }
+    __syncthreads();
+}
+// Peer step epilogue: this CTA's stores (local and peer) are visible system-wide; the last CTA signals.
+__device__ __forceinline__ void peer_done(const SmoothV4 &a) {
+    __threadfence_system();   // every thread fences its own stores
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long old = atomicAdd(a.peer.ctr, 1ull);
+        if (old == a.peer.ctr_last) {
+            __threadfence_system();
+            for (int s = 0; s < 2; ++s)
+                if (a.peer.side[s].dst) st_release_sys64(a.peer.side[s].peer_sig, a.peer.g + 1);
+        }
+    }
+}
+// Boundary layers also go straight into the neighbours' halos (peer step).
+__device__ __forceinline__ void peer_push(const SmoothV4 &a, uint32_t w, float4 r4) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const PeerSide &ps = a.peer.side[s];
+        if (ps.dst && w >= ps.src_begin && w < ps.src_end) ps.dst[ps.dst_begin + (w - ps.src_begin)] = r4;
+    }
+}
+
 template <bool PACKED, bool PREF = false, bool PEER = false, bool SPHERE = false>
 __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
-    if constexpr (PEER) {   // both neighbours finished iteration g - 1 (their halo pushes are here)
-        if (threadIdx.x == 0) {
-            const uint64_t t0 = globaltimer_ns();
-            for (int s = 0; s < 2; ++s) {
-                if (!a.peer.side[s].dst) continue;
-                while (ld_acquire_sys64(a.peer.sig + s) < a.peer.g) {
-                    if (globaltimer_ns() - t0 > kPeerTimeoutNs) {   // fail loudly: no smoothing on stale halos
-                        atomicExch(a.peer.err, 1u);
-                        __threadfence_system();
-                        __trap();
-                    }
-                    __nanosleep(64);
-                }
-            }
-        }
-        __syncthreads();
-    }
+    if constexpr (PEER) peer_wait(a);
     const float4 *__restrict__ src = a.src;
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t base0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -347,27 +371,10 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
         } else {
             const float4 r4 = make_float4(r.x, r.y, r.z, __uint_as_float(e_lo));   // w: split cache lo word
             st_stream_f4(a.dst + w, r4);
-            if constexpr (PEER) {   // boundary layers also go straight into the neighbours' halos
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const PeerSide &ps = a.peer.side[s];
-                    if (ps.dst && w >= ps.src_begin && w < ps.src_end) ps.dst[ps.dst_begin + (w - ps.src_begin)] = r4;
-                }
-            }
+            if constexpr (PEER) peer_push(a, w, r4);
         }
     }
-    if constexpr (PEER) {   // this CTA's stores (local and peer) are visible system-wide; the last CTA signals
-        __threadfence_system();   // every thread fences its own stores
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned long long old = atomicAdd(a.peer.ctr, 1ull);
-            if (old == a.peer.ctr_last) {
-                __threadfence_system();
-                for (int s = 0; s < 2; ++s)
-                    if (a.peer.side[s].dst) st_release_sys64(a.peer.side[s].peer_sig, a.peer.g + 1);
-            }
-        }
-    }
+    if constexpr (PEER) peer_done(a);
 }
 
 // Split smoothing cache, iterations 2..T of psn_smooth (whole volume, packed cache): the offsets'
@@ -377,10 +384,11 @@ __global__ void __launch_bounds__(256) k_smooth_v4(SmoothV4 a) {
 // 16 + 4 instead of 16 + 8 bytes per point (VERDICT r1 "use the w slot for useful data").  Same
 // update, same order: bit-identical to k_smooth_v4.  PREF loads the next grid-stride step's own
 // offsets and hi word one step ahead, so the neighbour gathers are the only loads on a step's path.
-template <bool PREF, bool SPHERE>
+template <bool PREF, bool SPHERE, bool PEER = false>
 __global__ void __launch_bounds__(256) k_smooth_split(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
+    if constexpr (PEER) peer_wait(a);
     const float4 *__restrict__ src = a.src;
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t base0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
@@ -388,7 +396,7 @@ __global__ void __launch_bounds__(256) k_smooth_split(SmoothV4 a) {
     uint32_t h_next = 0u;
     if (PREF && base0 < n) {
         const uint32_t ii = min(base0 + lane, n - 1u);
-        o_next = __ldg(src + a.halo_lo + ii); h_next = ld_stream_u32(a.hi + ii);
+        o_next = ld_src<PEER>(src + a.halo_lo + ii); h_next = ld_stream_u32(a.hi + ii);
     }
     for (uint32_t base = base0; base < n; base += stride) {
         const uint32_t i = base + lane;
@@ -401,23 +409,24 @@ __global__ void __launch_bounds__(256) k_smooth_split(SmoothV4 a) {
             o4 = o_next; hy = h_next;
             if (base + stride < n) {
                 const uint32_t jn = min(base + stride + lane, n - 1u);
-                o_next = __ldg(src + a.halo_lo + jn); h_next = ld_stream_u32(a.hi + jn);
+                o_next = ld_src<PEER>(src + a.halo_lo + jn); h_next = ld_stream_u32(a.hi + jn);
             }
         } else {
-            o4 = __ldg(src + w); hy = ld_stream_u32(a.hi + ii);
+            o4 = ld_src<PEER>(src + w); hy = ld_stream_u32(a.hi + ii);
         }
         const uint2 e = make_uint2(__float_as_uint(o4.w), hy);
         const uint32_t f = act ? nbr8_faces(e) : 0u;
         const uint4 nb = nbr8_idx(e, w);
-        const float4 h0 = __ldg(src + nb.x), h1 = __ldg(src + nb.y), h2 = __ldg(src + nb.z), h3 = __ldg(src + nb.w);
+        const float4 h0 = ld_src<PEER>(src + nb.x), h1 = ld_src<PEER>(src + nb.y), h2 = ld_src<PEER>(src + nb.z),
+                     h3 = ld_src<PEER>(src + nb.w);
         const float3 o = make_float3(o4.x, o4.y, o4.z);
         float3 mx, px;
         mx.x = __shfl_up_sync(kFull, o.x, 1); mx.y = __shfl_up_sync(kFull, o.y, 1); mx.z = __shfl_up_sync(kFull, o.z, 1);
         px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
         if (!act) continue;
         if (f) {
-            if ((f & 4u) && lane == 0) { const float4 v = __ldg(src + w - 1u); mx = make_float3(v.x, v.y, v.z); }
-            if ((f & 8u) && (lane == 31 || i + 1u >= n)) { const float4 v = __ldg(src + w + 1u); px = make_float3(v.x, v.y, v.z); }
+            if ((f & 4u) && lane == 0) { const float4 v = ld_src<PEER>(src + w - 1u); mx = make_float3(v.x, v.y, v.z); }
+            if ((f & 8u) && (lane == 31 || i + 1u >= n)) { const float4 v = ld_src<PEER>(src + w + 1u); px = make_float3(v.x, v.y, v.z); }
         }
         float3 r;
         if constexpr (SPHERE)
@@ -431,9 +440,12 @@ __global__ void __launch_bounds__(256) k_smooth_split(SmoothV4 a) {
             a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
             a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
         } else {
-            st_stream_f4(a.dst + w, make_float4(r.x, r.y, r.z, o4.w));
+            const float4 r4 = make_float4(r.x, r.y, r.z, o4.w);
+            st_stream_f4(a.dst + w, r4);
+            if constexpr (PEER) peer_push(a, w, r4);
         }
     }
+    if constexpr (PEER) peer_done(a);
 }
 
 // First Jacobi iteration of psn_smooth with the split cache, fused with the cache build (replaces

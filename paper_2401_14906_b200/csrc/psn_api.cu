@@ -951,9 +951,12 @@ psn_status psn_smooth_step(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *
     return cuda_check(ctx, "smooth step launch");
 }
 
-psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
-                                size_t ws_bytes, const float *src, float *dst, int parity, float relaxation,
-                                float constraint_distance, psn_peer *peer, void *stream) {
+namespace {
+// split: 0 = k_smooth_v4 with the 8-byte cache, 1 = the same writing the split cache (first step of a run;
+// hi -> its hi words), 2 = k_smooth_split reading it (later steps of the same psn_smooth_run_peer)
+psn_status step_peer_impl(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws, size_t ws_bytes,
+                          const float *src, float *dst, int parity, float relaxation, float constraint_distance,
+                          psn_peer *peer, void *stream, int split, uint32_t *hi) {
     if (!ctx) return PSN_ERR_ARG;
     ctx->launches = 0;
     psn_status s = check_smooth_args(ctx, mesh, relaxation, constraint_distance);
@@ -982,7 +985,11 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
         o.peer_sig = ps.peer_sig;
     }
     if (cudaSetDevice(ctx->device) != cudaSuccess) return cuda_check(ctx, "cudaSetDevice");
-    const V4Fn kern = pick_v4(smooth_packed(ctx, vol), false, true, ctx->constraint == PSN_CONSTRAINT_SPHERE);
+    const bool sph = ctx->constraint == PSN_CONSTRAINT_SPHERE;
+    const V4Fn kern = split == 2 ? (sph ? k_smooth_split<false, true, true> : k_smooth_split<false, false, true>)
+                                 : pick_v4(smooth_packed(ctx, vol), false, true, sph);
+    if (split == 1) v.hi_out = hi;
+    if (split == 2) v.hi = hi;
     const int64_t g4 = v4_grid(ctx, kern, mesh->n_points);
     v.peer.sig = peer->sig; v.peer.ctr = reinterpret_cast<unsigned long long *>(peer->ctr); v.peer.err = peer->err;
     v.peer.ctr_last = (unsigned long long)(peer->ctr_base + (uint64_t)g4 - 1);
@@ -993,6 +1000,25 @@ psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_m
     peer->ctr_base += (uint64_t)g4;
     peer->iteration += 1;
     return PSN_OK;
+}
+}  // namespace
+
+psn_status psn_smooth_step_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
+                                size_t ws_bytes, const float *src, float *dst, int parity, float relaxation,
+                                float constraint_distance, psn_peer *peer, void *stream) {
+    // test hook (PSN_PEER_STEP_SPLIT): step with the split cache as psn_smooth_run_peer does (src = NULL writes
+    // it, later steps read it), so single-process tests can interleave emulated ranks step by step
+    int split = 0;
+    uint32_t *hi = nullptr;
+    if (getenv("PSN_PEER_STEP_SPLIT") && mesh && vol && smooth_packed(ctx, vol) && mesh->n_points > 0) {
+        const size_t hi_at = align_up(8 * (size_t)mesh->n_points);
+        if (hi_at + 4 * (size_t)mesh->n_points <= smooth_layout(mesh).buf0) {
+            split = src ? 2 : 1;
+            hi = reinterpret_cast<uint32_t *>(static_cast<char *>(const_cast<void *>(ws)) + hi_at);
+        }
+    }
+    return step_peer_impl(ctx, vol, mesh, ws, ws_bytes, src, dst, parity, relaxation, constraint_distance, peer, stream,
+                          split, hi);
 }
 
 psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh, const void *ws,
@@ -1006,10 +1032,17 @@ psn_status psn_smooth_run_peer(psn_ctx *ctx, const psn_volume *vol, const psn_me
     // buffer parity continues from the global iteration (not from 0 per call): the first step of a later
     // run then writes the buffer the neighbour's previous run did NOT end in (the one its finalize reads)
     const uint64_t g0 = peer->iteration;
+    // split smoothing cache (as psn_smooth): the run's first step writes it, the later steps read it; its hi
+    // words live in the second half of the cache region (the packed cache uses 8 of its 16 bytes per point)
+    const int64_t n = mesh ? mesh->n_points : 0;
+    const size_t hi_at = align_up(8 * (size_t)std::max<int64_t>(n, 0));
+    const bool split = mesh && vol && smooth_packed(ctx, vol) && iterations > 1 && n > 0 &&
+                       hi_at + 4 * (size_t)n <= smooth_layout(mesh).buf0 && !getenv("PSN_SMOOTH_NOSPLIT");
+    uint32_t *hi = split ? reinterpret_cast<uint32_t *>(static_cast<char *>(const_cast<void *>(ws)) + hi_at) : nullptr;
     for (int32_t t = 0; t < iterations; ++t) {
         const int par = (int)((g0 + (uint64_t)t) & 1u);
-        const psn_status s = psn_smooth_step_peer(ctx, vol, mesh, ws, ws_bytes, t ? buf[par ^ 1] : nullptr,
-                                                  buf[par], par, relaxation, constraint_distance, peer, stream);
+        const psn_status s = step_peer_impl(ctx, vol, mesh, ws, ws_bytes, t ? buf[par ^ 1] : nullptr, buf[par], par,
+                                            relaxation, constraint_distance, peer, stream, split ? (t ? 2 : 1) : 0, hi);
         if (s != PSN_OK) return s;
         launches += ctx->launches;
     }

@@ -75,8 +75,13 @@ def volume():
     return a
 
 
-@pytest.mark.parametrize("G,shape", [(2, 0), (3, 0), (5, 0), (3, 1)])
-def test_peer_slabs_match_single(G, shape):
+@pytest.mark.parametrize("G,shape,split", [(2, 0, 0), (3, 0, 0), (5, 0, 0), (3, 1, 0), (2, 0, 1), (3, 0, 1), (5, 0, 1),
+                                           (3, 1, 1)])
+def test_peer_slabs_match_single(monkeypatch, G, shape, split):
+    """Peer-push slab smoothing equals one-GPU psn_smooth bit for bit -- with the 8-byte cache, and with the
+    split cache psn_smooth_run_peer uses (split: step 0 writes it, steps 1.. read it; PSN_PEER_STEP_SPLIT)."""
+    if split:
+        monkeypatch.setenv("PSN_PEER_STEP_SPLIT", "1")
     p = gu.psn()
     p.set_constraint(shape)   # box, or the sphere (reading Q26)
     try:
@@ -107,8 +112,10 @@ def _peer_slabs_match_single(p, G):
     np.testing.assert_array_equal(g["smoothed"], s1[:m1.n_points].cpu().numpy())
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_peer_balanced_shards_match_single(G):
+@pytest.mark.parametrize("G,split", [(2, 0), (4, 0), (2, 1), (4, 1)])
+def test_peer_balanced_shards_match_single(monkeypatch, G, split):
+    if split:   # the split cache psn_smooth_run_peer uses, stepped rank by rank
+        monkeypatch.setenv("PSN_PEER_STEP_SPLIT", "1")
     p = gu.psn()
     host = psn_gen.generate_host(psn_gen.config("c2"))[60:140]
     T, lam, d = 9, 0.5, 0.5
