@@ -454,9 +454,9 @@ def run_psn(args, rank, world, local_rank):
     per_launch_ms = t_v4 if t_v4 else t_sm / max(T, 1)
     sm_gbs = b_sm / (t_sm / max(T, 1) * 1e-3) / 1e9          # the smoothing half incl. the cache prep
     v4_gbs = b_sm / (per_launch_ms * 1e-3) / 1e9
-    # whole-volume psn_smooth (N = 1): iteration 1 is k_smooth_v4, iterations 2..T k_smooth_split (split cache);
-    # slabs / shards (N > 1) step with k_smooth_v4
-    sm_kern = "k_smooth_split" if (world == 1 and T > 1) else "k_smooth_v4"
+    # whole-volume psn_smooth (N = 1) and the peer-push run (N > 1): iterations 2..T are k_smooth_split (split
+    # cache); the NCCL-halo steps (--nccl-halo) are k_smooth_v4
+    sm_kern = "k_smooth_split" if (T > 1 and (world == 1 or halo_peer)) else "k_smooth_v4"
     dominant = sm_kern if t_sm >= t_ext else "extraction (k_count3+k_scan+k_emit_band)"
     roof = {"bound": "hbm", "kernel": sm_kern, "achieved": v4_gbs / world, "peak": peak, "unit": "GB/s",
             "frac": v4_gbs / world / peak, "traffic": profile_traffic(sm_kern, cfg), "peak_source": peak_src,
