@@ -828,7 +828,7 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         // the point's own offsets and its hi word from a 4-byte array in the cache region's second half
         // (free: the packed cache uses 8 of the 16 bytes per point the region holds)
         uint32_t *hi = split ? at<uint32_t>(ws, hi_at) : nullptr;
-        const V4Fn kern2 = split ? split_sel(pref && !getenv("PSN_SPLIT_NOPREF"), cons.sphere != 0) : kern;
+        const V4Fn kern2 = split ? split_sel(pref, cons.sphere != 0) : kern;
         const int64_t g42 = split ? v4_grid(ctx, kern2, nw) : g4;
         const float4 *s4 = nullptr;
         if (ctx->smooth_ev[0]) record_event(ctx->smooth_ev[0], st);
