@@ -490,6 +490,64 @@ __global__ void __launch_bounds__(256) k_smooth_first(SmoothV4 a) {
     }
 }
 
+// Iterations 1 AND 2 of psn_smooth in one pass (split cache, whole volume).  Before iteration 1 every
+// offset is zero, so a point's iteration-1 offset is a function of its face mask alone (Eq. 1 with all
+// neighbour terms zero): the kernel tabulates it for the 64 masks with the same update code, then computes
+// iteration 2 from the point's own and its six neighbours' face masks -- the values the stored-and-reloaded
+// iteration-1 offsets would hold, bit for bit (fp32 stores and loads are exact) -- while building the split
+// cache from the CSR stencil as k_smooth_first does.  One pass of 1 + 4 + 4S/P + ~4 (neighbour masks) bytes
+// read and 20 written per point replaces k_smooth_first's pass plus one k_smooth_split pass.
+template <bool SPHERE>
+__global__ void __launch_bounds__(256) k_smooth_first2(SmoothV4 a) {
+    __shared__ float3 tab[64];
+    const float3 z = make_float3(0.f, 0.f, 0.f);
+    for (int f = threadIdx.x; f < 64; f += blockDim.x) {
+        if constexpr (SPHERE) tab[f] = jacobi_update_t<true>((uint32_t)f, z, z, z, z, z, z, z, a.lambda, a.cons);
+        else tab[f] = jacobi_update_box((uint32_t)f, z, z, z, z, z, z, z, a.lambda, a.d);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = a.n_own;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const uint32_t i = base + lane;
+        const bool act = i < n;
+        const uint32_t ii = act ? i : n - 1u;
+        const uint32_t w = a.halo_lo + ii;   // whole volume: halo_lo = 0, window index = own index
+        const uint32_t fm = a.fmask[ii];
+        uint32_t s = __ldg(a.csr_off + ii) - a.first_stencil;
+        uint4 v = make_uint4(w, w, w, w);
+        if (fm & 1u) v.x = __ldg(a.csr_ids + s++) - a.win_base;    // -z
+        if (fm & 2u) v.y = __ldg(a.csr_ids + s++) - a.win_base;    // -y
+        if (fm & 4u) ++s;                                          // -x  (w - 1)
+        if (fm & 8u) ++s;                                          // +x  (w + 1)
+        if (fm & 16u) v.z = __ldg(a.csr_ids + s++) - a.win_base;   // +y
+        if (fm & 32u) v.w = __ldg(a.csr_ids + s++) - a.win_base;   // +z
+        const uint2 e = nbr8_pack(w, v, fm);
+        const uint32_t f = nbr8_faces(e);
+        const float3 o = tab[f];
+        float3 mx, px;
+        mx.x = __shfl_up_sync(kFull, o.x, 1); mx.y = __shfl_up_sync(kFull, o.y, 1); mx.z = __shfl_up_sync(kFull, o.z, 1);
+        px.x = __shfl_down_sync(kFull, o.x, 1); px.y = __shfl_down_sync(kFull, o.y, 1); px.z = __shfl_down_sync(kFull, o.z, 1);
+        if (!act) continue;
+        if ((f & 4u) && lane == 0) mx = tab[a.fmask[w - 1u - a.halo_lo]];
+        if ((f & 8u) && (lane == 31 || i + 1u >= n)) px = tab[a.fmask[w + 1u - a.halo_lo]];
+        const float3 g0 = tab[(f & 1u) ? a.fmask[v.x - a.halo_lo] : fm], g1 = tab[(f & 2u) ? a.fmask[v.y - a.halo_lo] : fm];
+        const float3 g2 = tab[(f & 16u) ? a.fmask[v.z - a.halo_lo] : fm], g3 = tab[(f & 32u) ? a.fmask[v.w - a.halo_lo] : fm];
+        float3 r;
+        if constexpr (SPHERE) r = jacobi_update_t<true>(f, o, mx, px, g0, g1, g2, g3, a.lambda, a.cons);
+        else r = jacobi_update_box(f, o, mx, px, g0, g1, g2, g3, a.lambda, a.d);
+        if (a.world) {
+            a.world[3u * w + 0u] = world_of(__ldg(a.points + 3u * w + 0u), r.x, a.org[0], a.sp[0]);
+            a.world[3u * w + 1u] = world_of(__ldg(a.points + 3u * w + 1u), r.y, a.org[1], a.sp[1]);
+            a.world[3u * w + 2u] = world_of(__ldg(a.points + 3u * w + 2u), r.z, a.org[2], a.sp[2]);
+        } else {
+            st_stream_f4(a.dst + w, make_float4(r.x, r.y, r.z, __uint_as_float(e.x)));
+            st_stream_u32(a.hi_out + ii, e.y);
+        }
+    }
+}
+
 // World coordinates of window entries [w0, w1) from float4 offsets (NULL = anchors).
 __global__ void __launch_bounds__(256) k_finalize(const float4 *offs, const float *points, float *out,
                                                   int64_t w0, int64_t w1, double sx, double sy, double sz,

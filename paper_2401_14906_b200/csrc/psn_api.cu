@@ -832,7 +832,20 @@ psn_status psn_smooth(psn_ctx *ctx, const psn_volume *vol, const psn_mesh *mesh,
         const int64_t g42 = split ? v4_grid(ctx, kern2, nw) : g4;
         const float4 *s4 = nullptr;
         if (ctx->smooth_ev[0]) record_event(ctx->smooth_ev[0], st);
-        for (int32_t t = 0; t < iterations; ++t) {
+        int32_t t_begin = 0;
+        if (first && !getenv("PSN_SMOOTH_NOFIRST2")) {   // iterations 1 and 2 in one pass (k_smooth_first2)
+            const bool last = iterations == 2;
+            v.src = nullptr; v.dst = last ? nullptr : b4[1]; v.world = last ? out : nullptr; v.hi_out = hi;
+            v.fmask = mesh->face_masks; v.csr_off = mesh->stencil_offsets; v.csr_ids = mesh->stencil_ids;
+            v.win_base = (uint32_t)(mesh->first_point - mesh->halo_lo_points);
+            v.first_stencil = (uint32_t)mesh->first_stencil;
+            const V4Fn f2 = cons.sphere ? k_smooth_first2<true> : k_smooth_first2<false>;
+            f2<<<(unsigned)v4_grid(ctx, f2, nw), 256, 0, st>>>(v);
+            ++ctx->launches;
+            s4 = v.dst;
+            t_begin = 2;
+        }
+        for (int32_t t = t_begin; t < iterations; ++t) {
             const bool last = (t == iterations - 1);
             v.src = s4; v.dst = last ? nullptr : b4[t & 1]; v.world = last ? out : nullptr;
             v.hi_out = (split && t == 0) ? hi : nullptr; v.hi = hi;

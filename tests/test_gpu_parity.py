@@ -363,7 +363,8 @@ def test_split_smoothing_cache_bit_identical(monkeypatch, sphere):
     """Iterations 2..T with the split cache (k_smooth_split: the packed entry's lo word in the
     offsets' w slot, the hi word in a 4-byte array) give the same bits as k_smooth_v4 reading
     the 8-byte entries every iteration -- emitted cache, prep-built cache, and the cache built
-    by the first iteration itself (k_smooth_first); T = 1, 2, 3, 9, box and sphere constraints,
+    by the first iteration itself (k_smooth_first), and iterations 1 + 2 in one pass from the face
+    masks (k_smooth_first2); T = 1, 2, 3, 9, box and sphere constraints,
     and a mesh too small for the split (it falls back)."""
     p = gu.psn()
     rng = np.random.default_rng(91)
@@ -385,7 +386,10 @@ def test_split_smoothing_cache_bit_identical(monkeypatch, sphere):
             for T in (1, 2, 3, 9):
                 for cached in (1, 0):
                     mesh.c.smooth_cache_valid = cached
-                    split = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()   # cached=0: k_smooth_first
+                    split = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()   # cached=0: k_smooth_first2
+                    monkeypatch.setenv("PSN_SMOOTH_NOFIRST2", "1")
+                    split1 = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()  # k_smooth_first + split
+                    monkeypatch.delenv("PSN_SMOOTH_NOFIRST2")
                     monkeypatch.setenv("PSN_SMOOTH_NOFIRST", "1")
                     split_prep = p.smooth(vol, mesh, T, 0.5, 0.5, ws=ws).clone()   # k_smooth_prep8 + split
                     monkeypatch.delenv("PSN_SMOOTH_NOFIRST")
@@ -394,6 +398,7 @@ def test_split_smoothing_cache_bit_identical(monkeypatch, sphere):
                     monkeypatch.delenv("PSN_SMOOTH_NOSPLIT")
                     assert torch.equal(split[:n], plain[:n]), (a.shape, T, cached)
                     assert torch.equal(split_prep[:n], plain[:n]), (a.shape, T, cached)
+                    assert torch.equal(split1[:n], plain[:n]), (a.shape, T, cached)
                 mesh.c.smooth_cache_valid = 1
     finally:
         p.set_constraint(0)
