@@ -509,13 +509,22 @@ __global__ void __launch_bounds__(256) k_smooth_first2(SmoothV4 a) {
     const int lane = threadIdx.x & 31;
     const uint32_t n = a.n_own;
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+    // the next grid-stride step's face mask and CSR offset are loaded one step ahead (as k_smooth_first;
+    // c4 -0.8 %, c3 -0.6 %, c6 -0.6 %)
+    uint32_t fm_n = 0u, so_n = 0u;
+    if (base < n) { const uint32_t j = min(base + lane, n - 1u); fm_n = a.fmask[j]; so_n = __ldg(a.csr_off + j); }
+    for (; base < n; base += stride) {
         const uint32_t i = base + lane;
         const bool act = i < n;
         const uint32_t ii = act ? i : n - 1u;
         const uint32_t w = a.halo_lo + ii;   // whole volume: halo_lo = 0, window index = own index
-        const uint32_t fm = a.fmask[ii];
-        uint32_t s = __ldg(a.csr_off + ii) - a.first_stencil;
+        const uint32_t fm = fm_n;
+        uint32_t s = so_n - a.first_stencil;
+        if (base + stride < n) {
+            const uint32_t j = min(base + stride + lane, n - 1u);
+            fm_n = a.fmask[j]; so_n = __ldg(a.csr_off + j);
+        }
         uint4 v = make_uint4(w, w, w, w);
         if (fm & 1u) v.x = __ldg(a.csr_ids + s++) - a.win_base;    // -z
         if (fm & 2u) v.y = __ldg(a.csr_ids + s++) - a.win_base;    // -y
